@@ -1,0 +1,154 @@
+/*
+ * ternkit_b200.h -- C-ABI of the B200 (sm_100a) ternary hot path.
+ *
+ * Drop-in boundary for the reference's header-only API (ternkit, R: =
+ * /root/reference/proj/include/ternkit/).  The reference has no plugin
+ * registry: its public C++ functions ARE the interface, so each entry point
+ * below names the reference function it replaces.  The C++ shim
+ * include/ternkit_b200/ternkit.hpp re-exposes exactly those C++ signatures
+ * (host spans in, value-type results out, std::invalid_argument on error) on
+ * top of this C layer; Python reaches it through ctypes
+ * (paper_2008_05101_b200/_lib.py).
+ *
+ * Conventions
+ *  - Buffers are caller-owned DEVICE pointers unless a parameter says _host.
+ *  - Calls are asynchronous on `stream` (a cudaStream_t, NULL = legacy
+ *    default stream) and return a status immediately for argument errors.
+ *  - Data-dependent errors (non-finite input, negative activation -- the
+ *    reference's throws in R:quantizer.hpp:37-41,53-55) are raised inside the
+ *    kernels into the context's device error word; tk_context_sync() waits
+ *    for the stream and returns the FIRST such error in the reference's
+ *    evaluation order, then clears it.
+ *  - One context per concurrently used stream (the context owns scratch).
+ *  - Packed words are the reference layout byte for byte: 32 lanes per u64,
+ *    lane i at bits 2(i%32), padding lanes 0b01 (R:codec.hpp:14-20).
+ */
+#ifndef TERNKIT_B200_H
+#define TERNKIT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (all map to std::invalid_argument in the C++ shim) ---- */
+#define TK_OK 0
+#define TK_ERR_INVALID 1           /* length / shape / geometry mismatch      */
+#define TK_ERR_THRESHOLDS 3        /* alpha1/alpha2 not > 0, R:codec.hpp:61   */
+#define TK_ERR_NONFINITE 4         /* R:quantizer.hpp:37-41                   */
+#define TK_ERR_NEGATIVE 5          /* R:quantizer.hpp:53-55                   */
+#define TK_ERR_OFFSET_SYMMETRIC 6  /* R:linalg.hpp:245-249                    */
+#define TK_ERR_MASKS 7             /* R:linalg.hpp:242-244                    */
+#define TK_ERR_RANGE 8             /* value outside {-1,0,1}, R:codec.hpp:49  */
+#define TK_ERR_CUDA 9              /* CUDA runtime failure                    */
+#define TK_ERR_UNSUPPORTED 10      /* backend cannot run this shape           */
+
+#define TK_MODE_WEIGHT 0             /* QuantMode::kWeight                   */
+#define TK_MODE_ACTIVATION_NONNEG 1  /* QuantMode::kActivationNonneg         */
+
+#define TK_MASK_ON_THE_FLY 0   /* MaskMode::kOnTheFly                         */
+#define TK_MASK_PRECOMPUTED 1  /* MaskMode::kPrecomputed                      */
+
+#define TK_BACKEND_AUTO 0    /* per-shape choice (profiles/)       */
+#define TK_BACKEND_POPC 1    /* LOP3 + POPC integer pipe                      */
+#define TK_BACKEND_TC_I8 2   /* tcgen05.mma kind::i8 tensor cores             */
+
+typedef struct tk_context tk_context;
+typedef struct tk_layer tk_layer;
+
+int tk_version(void);
+const char* tk_status_string(int status);
+
+/* ---- context ------------------------------------------------------------ */
+int tk_context_create(int device, tk_context** out);
+int tk_context_destroy(tk_context* ctx);
+/* Waits for `stream`, returns the first in-kernel error (or TK_OK), clears it. */
+int tk_context_sync(tk_context* ctx, void* stream);
+
+/* Exact float thresholds equivalent to the reference quantizer
+ * (R:quantizer.hpp:44-60): lane bit0 = (p > t0), bit1 = (p > t1).  Host-only
+ * helper, exposed so the threshold search can be tested without a GPU. */
+int tk_quant_thresholds(float alpha1, float alpha2, int mode, float* t0,
+                        float* t1);
+
+/* fuse_bn(mean, var, gamma, beta, eps) -> ChannelAffine  R:linalg.hpp:70-91
+ * Host-side parameter folding (one-time layer prep, host arrays), with the
+ * reference build's float semantics (its multiply-subtract is one FMA). */
+int tk_fuse_bn(const float* mean_host, const float* var_host,
+               const float* gamma_host, const float* beta_host, float eps,
+               int channels, float* gain_host, float* bias_host);
+
+/* ---- codec / quantizer (R:codec.hpp, R:quantizer.hpp) ------------------- */
+/* pack(span<const int8_t>)                         R:codec.hpp:89-100 */
+int tk_pack(tk_context* ctx, const int8_t* values, size_t n, uint64_t* words,
+            void* stream);
+/* unpack(PackedTernaryVector)                      R:codec.hpp:107-117 */
+int tk_unpack(tk_context* ctx, const uint64_t* words, size_t n, int8_t* values,
+              void* stream);
+/* quantize_and_pack(span<const float>, thr, mode)  R:quantizer.hpp:159-170
+ * `rows` independent vectors of `n` floats each, row r packed into
+ * words[r * words_for_lanes(n) ...]. */
+int tk_quantize_pack(tk_context* ctx, const float* x, size_t rows, size_t n,
+                     float alpha1, float alpha2, int mode, uint64_t* words,
+                     void* stream);
+
+/* ---- inner products (R:bitkernels.hpp) ---------------------------------- */
+/* out[p] = ternary_dot(x_p, y_p) (+ wsum[p] if wsum != NULL, i.e.
+ * ternary_dot_nonneg).  x,y: [pairs][words] u64.    R:bitkernels.hpp:116-159 */
+int tk_ternary_dot_batched(tk_context* ctx, const uint64_t* x,
+                           const uint64_t* y, size_t words, size_t pairs,
+                           const int64_t* wsum, int64_t* out, void* stream);
+
+/* ---- linalg (R:linalg.hpp) ---------------------------------------------- */
+/* im2col_quantize_pack(x NCHW, shape, thr, geom, mode)  R:linalg.hpp:173-225
+ * rows: [n*oh*ow][words_for_lanes(c*kh*kw)] u64. */
+int tk_im2col_quantize_pack(tk_context* ctx, const float* x, int n, int c,
+                            int h, int w, int kh, int kw, int stride, int pad,
+                            float alpha1, float alpha2, int mode,
+                            uint64_t* rows, void* stream);
+
+/* make_packed_conv_layer(int8 weights, geom, thr_w, thr_a, nonneg, fused,
+ * out_scale)                                         R:linalg.hpp:118-144
+ * weights_host: [out_c][in_c*kh*kw] in {-1,0,1}; gain/bias_host may be NULL
+ * (identity affine, R:linalg.hpp:133-134).  Uploads packed rows, weight sums,
+ * zero masks and the int8 tensor-core operand once. */
+int tk_layer_create(tk_context* ctx, const int8_t* weights_host, int in_c,
+                    int out_c, int kh, int kw, int stride, int pad,
+                    float tw1, float tw2, float ta1, float ta2,
+                    int activation_nonneg, const float* gain_host,
+                    const float* bias_host, float out_scale, tk_layer** out);
+int tk_layer_destroy(tk_layer* layer);
+/* PackedConvLayer::precompute_masks()                R:linalg.hpp:109-113 */
+int tk_layer_precompute_masks(tk_layer* layer);
+int tk_layer_set_backend(tk_layer* layer, int backend);
+int tk_layer_get_backend(const tk_layer* layer, int m_rows);
+/* host copies of the packed rows / weight sums (PackedConvLayer::weights,
+ * ::weight_sums) for callers that inspect them */
+int tk_layer_words_host(const tk_layer* layer, uint64_t* words_host,
+                        int32_t* wsums_host);
+
+/* packed_gemm(Im2colBuffer, layer, mask_mode, workers) R:linalg.hpp:232-293
+ * rows: [row_count][words_for_lanes(row_len)] u64; out: [row_count][out_c]. */
+int tk_packed_gemm(tk_context* ctx, const tk_layer* layer,
+                   const uint64_t* rows, size_t row_count, size_t row_len,
+                   int nonneg_offset, int mask_mode, int32_t* out,
+                   void* stream);
+
+/* conv2d_ternary(x NCHW, shape, layer, mask_mode, workers)
+ *                                                    R:linalg.hpp:301-328
+ * out: [n][out_c][oh][ow] f32 = gain*(out_scale*acc)+bias (one FMA). */
+int tk_conv2d_ternary(tk_context* ctx, const tk_layer* layer, const float* x,
+                      int n, int h, int w, int mask_mode, float* out,
+                      void* stream);
+
+/* fully_connected_ternary(x, batch, layer, mask_mode) R:linalg.hpp:332-343 */
+int tk_fully_connected_ternary(tk_context* ctx, const tk_layer* layer,
+                               const float* x, int batch, int mask_mode,
+                               float* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

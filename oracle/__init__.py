@@ -1,0 +1,1 @@
+"""Parity checkers (TEST INFRASTRUCTURE ONLY -- see oracle/oracle.py)."""

@@ -1,0 +1,213 @@
+// tk_popc.cu -- the LOP3 + POPC integer-pipe path.
+//
+// Ternary multiply (R:bitkernels.hpp:55-63) on a word pair is
+//   TM(x, y) = (~(x ^ y) | d) & ~(d << 1),  d = (y ^ y >> 1) & kAuxi,
+// and for every lane popcount(TM) = popcount(~(x^y) & M) + [lane of y is 0]
+// with M = ~(d | d << 1).  Summed over a row:
+//   dot = sum_w popc(~(x_w ^ y_w) & M_w) + Z_y - 32 * words
+// where Z_y counts the zero lanes of the weight row (padding included).
+// M and Z are per weight row, precomputed once at layer creation, so the
+// inner loop is one LOP3 + one POPC + half an IADD3 per u32 word.
+#include "tk_internal.cuh"
+
+namespace {
+
+__device__ __forceinline__ uint32_t tm_u32(uint32_t x, uint32_t y) {
+  const uint32_t d = (y ^ (y >> 1)) & TK_KAUXI32;
+  return (~(x ^ y) | d) & ~(d << 1);
+}
+
+// cfg1: one warp per vector pair, R:bitkernels.hpp:76-85 (+ :151-159).
+__global__ void k_dot_batched(const uint4* __restrict__ x,
+                              const uint4* __restrict__ y, size_t words,
+                              size_t pairs, const int64_t* __restrict__ wsum,
+                              int64_t* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const size_t warp = (blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5;
+  const size_t nwarps = ((size_t)gridDim.x * blockDim.x) >> 5;
+  const size_t q = words / 2;  // uint4 = 2 u64 words
+  for (size_t p = warp; p < pairs; p += nwarps) {
+    const uint4* xp = x + p * q;
+    const uint4* yp = y + p * q;
+    int acc = 0;
+#pragma unroll 4
+    for (size_t i = lane; i < q; i += 32) {
+      const uint4 a = __ldg(xp + i), b = __ldg(yp + i);
+      acc += __popc(tm_u32(a.x, b.x)) + __popc(tm_u32(a.y, b.y)) +
+             __popc(tm_u32(a.z, b.z)) + __popc(tm_u32(a.w, b.w));
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) {
+      int64_t r = (int64_t)acc - (int64_t)words * 32;
+      out[p] = wsum ? r + wsum[p] : r;
+    }
+  }
+}
+
+// odd word counts: scalar u64 variant
+__global__ void k_dot_batched_u64(const uint64_t* __restrict__ x,
+                                  const uint64_t* __restrict__ y, size_t words,
+                                  size_t pairs, const int64_t* __restrict__ wsum,
+                                  int64_t* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const size_t warp = (blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5;
+  const size_t nwarps = ((size_t)gridDim.x * blockDim.x) >> 5;
+  for (size_t p = warp; p < pairs; p += nwarps) {
+    int acc = 0;
+    for (size_t i = lane; i < words; i += 32) {
+      const uint64_t a = x[p * words + i], b = y[p * words + i];
+      acc += __popc(tm_u32((uint32_t)a, (uint32_t)b)) +
+             __popc(tm_u32((uint32_t)(a >> 32), (uint32_t)(b >> 32)));
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) {
+      int64_t r = (int64_t)acc - (int64_t)words * 32;
+      out[p] = wsum ? r + wsum[p] : r;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Register-tiled packed GEMM: C[m][n] = sum_k popc(~(A[m][k]^B[n][k]) & M[n][k])
+// + cst[n].  CTA tile 64 x 64, 256 threads, 4 x 4 outputs per thread, K staged
+// through shared memory 16 u32 words at a time (k-major so each thread reads
+// its 4 rows / 4 columns with one LDS.128).  R:linalg.hpp:232-293.
+constexpr int BM = 64, BN = 64, BK = 16;
+
+__global__ void __launch_bounds__(256)
+k_gemm_popc(const uint32_t* __restrict__ A, int M, int K32,
+            const uint32_t* __restrict__ B, const uint32_t* __restrict__ Mk,
+            int N, const int32_t* __restrict__ wsum,
+            const int32_t* __restrict__ zcnt, int offset, tk_epilogue e) {
+  __shared__ __align__(16) uint32_t As[BK][BM];
+  __shared__ __align__(16) uint32_t Bs[BK][BN];
+  __shared__ __align__(16) uint32_t Ms[BK][BN];
+
+  const int tid = threadIdx.x;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const int tx = tid & 15, ty = tid >> 4;  // 16 x 16 threads
+  const int lr = tid >> 2, lk = (tid & 3) * 4;  // loader: row, k quad
+
+  int acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0;
+
+  const bool vec = (K32 % 4) == 0;
+  for (int k0 = 0; k0 < K32; k0 += BK) {
+    // ---- load tiles (zero outside the matrix: popc(~(0^0)&0) = 0) ----
+    uint32_t a4[4] = {0, 0, 0, 0}, b4[4] = {0, 0, 0, 0}, m4[4] = {0, 0, 0, 0};
+    const int gm = m0 + lr, gn = n0 + lr, gk = k0 + lk;
+    if (vec && gk + 3 < K32) {
+      if (gm < M) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(A + (size_t)gm * K32 + gk));
+        a4[0] = v.x; a4[1] = v.y; a4[2] = v.z; a4[3] = v.w;
+      }
+      if (gn < N) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(B + (size_t)gn * K32 + gk));
+        const uint4 u = __ldg(reinterpret_cast<const uint4*>(Mk + (size_t)gn * K32 + gk));
+        b4[0] = v.x; b4[1] = v.y; b4[2] = v.z; b4[3] = v.w;
+        m4[0] = u.x; m4[1] = u.y; m4[2] = u.z; m4[3] = u.w;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        if (gk + i < K32) {
+          if (gm < M) a4[i] = A[(size_t)gm * K32 + gk + i];
+          if (gn < N) {
+            b4[i] = B[(size_t)gn * K32 + gk + i];
+            m4[i] = Mk[(size_t)gn * K32 + gk + i];
+          }
+        }
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      As[lk + i][lr] = a4[i];
+      Bs[lk + i][lr] = b4[i];
+      Ms[lk + i][lr] = m4[i];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < BK; ++k) {
+      const uint4 a = *reinterpret_cast<const uint4*>(&As[k][ty * 4]);
+      const uint4 b = *reinterpret_cast<const uint4*>(&Bs[k][tx * 4]);
+      const uint4 m = *reinterpret_cast<const uint4*>(&Ms[k][tx * 4]);
+      const uint32_t av[4] = {a.x, a.y, a.z, a.w};
+      const uint32_t bv[4] = {b.x, b.y, b.z, b.w};
+      const uint32_t mv[4] = {m.x, m.y, m.z, m.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          acc[i][j] += __popc(~(av[i] ^ bv[j]) & mv[j]);
+    }
+  }
+
+  // ---- epilogue ----
+  const int words64 = K32 / 2;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int n = n0 + tx * 4 + j;
+    if (n >= N) continue;
+    const int cst = zcnt[n] - 32 * words64 + (offset ? wsum[n] : 0);
+    const float g = e.gain ? e.gain[n] : 1.0f;
+    const float bb = e.bias ? e.bias[n] : 0.0f;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int m = m0 + ty * 4 + i;
+      if (m >= M) continue;
+      const int v = acc[i][j] + cst;
+      if (e.mode == TK_EPI_I32) {
+        static_cast<int32_t*>(e.out)[(size_t)m * N + n] = v;
+      } else {
+        // R:linalg.hpp:322-323, contracted to one FMA like the reference build
+        const float y = __fmaf_rn(g, __fmul_rn(e.out_scale, (float)v), bb);
+        if (e.mode == TK_EPI_F32_ROWS) {
+          static_cast<float*>(e.out)[(size_t)m * N + n] = y;
+        } else {
+          const int b = m / e.plane, p = m - b * e.plane;
+          static_cast<float*>(e.out)[((size_t)b * N + n) * e.plane + p] = y;
+        }
+      }
+    }
+  }
+}
+
+}  // namespace
+
+cudaError_t tk_launch_dot_batched(const uint64_t* x, const uint64_t* y,
+                                  size_t words, size_t pairs,
+                                  const int64_t* wsum, int64_t* out,
+                                  cudaStream_t s) {
+  if (pairs == 0) return cudaSuccess;
+  size_t blocks = (pairs + 7) / 8;  // 8 warps per block
+  if (blocks > 148u * 32u) blocks = 148u * 32u;
+  const bool vec = words % 2 == 0 && ((uintptr_t)x % 16 == 0) &&
+                   ((uintptr_t)y % 16 == 0);
+  if (vec) {
+    k_dot_batched<<<(unsigned)blocks, 256, 0, s>>>(
+        reinterpret_cast<const uint4*>(x), reinterpret_cast<const uint4*>(y),
+        words, pairs, wsum, out);
+  } else {
+    k_dot_batched_u64<<<(unsigned)blocks, 256, 0, s>>>(x, y, words, pairs,
+                                                      wsum, out);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t tk_launch_gemm_popc(const uint64_t* rows, size_t M, int wpr64,
+                                const tk_layer* L, int offset, tk_epilogue e,
+                                cudaStream_t s) {
+  if (M == 0) return cudaSuccess;
+  dim3 grid((L->out_c + BN - 1) / BN, (unsigned)((M + BM - 1) / BM));
+  k_gemm_popc<<<grid, 256, 0, s>>>(
+      reinterpret_cast<const uint32_t*>(rows), (int)M, 2 * wpr64,
+      reinterpret_cast<const uint32_t*>(L->d_words), L->d_mask, L->out_c,
+      L->d_wsum, L->d_zcnt, offset, e);
+  return cudaGetLastError();
+}

@@ -1,0 +1,192 @@
+"""GPU parity: im2col_quantize_pack, packed_gemm, conv2d_ternary and
+fully_connected_ternary vs the reference's golden outputs and the C oracle,
+on both pipes (LOP3+POPC and tcgen05 kind::i8).  Integers and packed words
+bit-exact; float epilogue bit-exact (same FMA shape as the reference build)."""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def u64(t):
+    return t.detach().cpu().numpy().view(np.uint64)
+
+
+def backends(tk):
+    return [tk.Backend.POPC, tk.Backend.TC_I8]
+
+
+def _layer(tk, wq, c, oc, k, s, p, ta=(0.5, 0.9), nonneg=True, gain=None, bias=None, out_scale=1.0,
+           tw=(1.0, 1.0)):
+    g = tk.ConvGeometry(c, oc, k, k, s, p)
+    aff = None if gain is None else tk.ChannelAffine(gain, bias)
+    return tk.make_packed_conv_layer(wq, g, tk.QuantThresholds(*tw), tk.QuantThresholds(*ta), nonneg,
+                                     aff, out_scale)
+
+
+def test_im2col_kats(tk, golden):
+    QT, QM, TS, CG = tk.QuantThresholds, tk.QuantMode, tk.TensorShape, tk.ConvGeometry
+    b = tk.im2col_quantize_pack(golden["im2col_1x1_x"], TS(1, 3, 2, 2), QT(1, 1), CG(3, 1, 1, 1, 1, 0),
+                                QM.kWeight)
+    assert b.row_count == 4 and b.row_len == 3
+    assert np.array_equal(u64(b.words), golden["im2col_1x1_rows"])
+    b = tk.im2col_quantize_pack(np.ones(9, np.float32), TS(1, 1, 3, 3), QT(1, 1), CG(1, 1, 3, 3, 1, 1),
+                                QM.kWeight)
+    assert np.array_equal(u64(b.words), golden["im2col_corner_rows"])
+    b = tk.im2col_quantize_pack(golden["im2col_strided_x"], TS(2, 3, 5, 4), QT(0.6, 1.1),
+                                CG(3, 2, 3, 3, 2, 1), QM.kActivationNonneg)
+    assert b.nonneg_offset and np.array_equal(u64(b.words), golden["im2col_strided_rows"])
+    with pytest.raises(tk.InvalidArgument):   # channel mismatch, R:tests/test_linalg.cpp:165-175
+        tk.im2col_quantize_pack(np.zeros(32, np.float32), TS(1, 2, 4, 4), QT(1, 1), CG(3, 1, 3, 3, 1, 1),
+                                QM.kWeight)
+    with pytest.raises(tk.InvalidArgument):
+        tk.im2col_quantize_pack(np.zeros(3, np.float32), TS(1, 2, 4, 4), QT(1, 1), CG(2, 1, 3, 3, 1, 1),
+                                QM.kWeight)
+
+
+@pytest.mark.parametrize("backend", ["POPC", "TC_I8"])
+def test_conv_shapes_golden(tk, golden, backend):
+    QT, QM, TS, CG = tk.QuantThresholds, tk.QuantMode, tk.TensorShape, tk.ConvGeometry
+    for i, (c, r, k, s, p, b) in enumerate(golden["conv_shapes"]):
+        c, r, k, s, p, b = map(int, (c, r, k, s, p, b))
+        buf = tk.im2col_quantize_pack(golden[f"conv{i}_x"], TS(b, c, r, r), QT(0.5, 0.9), CG(c, c, k, k, s, p),
+                                      QM.kActivationNonneg)
+        assert np.array_equal(u64(buf.words), golden[f"conv{i}_rows"]), i
+        layer = _layer(tk, golden[f"conv{i}_w"], c, c, k, s, p, gain=golden[f"conv{i}_gain"],
+                       bias=golden[f"conv{i}_bias"], out_scale=0.37, tw=(0.8, 1.2))
+        layer.set_backend(tk.Backend[backend])
+        acc = tk.packed_gemm(buf, layer).cpu().numpy()
+        assert np.array_equal(acc, golden[f"conv{i}_acc"]), (i, backend)
+        y = tk.conv2d_ternary(golden[f"conv{i}_x"], TS(b, c, r, r), layer).data.cpu().numpy()
+        assert np.array_equal(y.view(np.int32), golden[f"conv{i}_y"].view(np.int32)), (i, backend)
+        # symmetric activations through a symmetric layer
+        lsym = _layer(tk, golden[f"conv{i}_w"], c, c, k, s, p, ta=(0.8, 1.2), nonneg=False)
+        lsym.set_backend(tk.Backend[backend])
+        bs = tk.im2col_quantize_pack(golden[f"conv{i}_xs"], TS(b, c, r, r), QT(0.8, 1.2), CG(c, c, k, k, s, p),
+                                     QM.kWeight)
+        assert np.array_equal(tk.packed_gemm(bs, lsym).cpu().numpy(), golden[f"conv{i}_acc_sym"]), (i, backend)
+        with pytest.raises(tk.InvalidArgument):   # offset rows into a symmetric layer
+            tk.packed_gemm(buf, lsym)
+
+
+def test_gemm_mask_modes_and_errors(tk, oracle):
+    """R:tests/test_linalg.cpp:215-231: precomputed mode requires masks; modes agree."""
+    rng = np.random.default_rng(38)
+    wq = rng.integers(-1, 2, (64, 32)).astype(np.int8)
+    layer = _layer(tk, wq, 32, 64, 1, 1, 0, ta=(0.5, 0.5))
+    x = np.abs(rng.standard_normal(10 * 32)).astype(np.float32)
+    buf = tk.im2col_quantize_pack(x, tk.TensorShape(10, 32, 1, 1), tk.QuantThresholds(0.5, 0.5),
+                                  layer.geom, tk.QuantMode.kActivationNonneg)
+    with pytest.raises(tk.InvalidArgument):
+        tk.packed_gemm(buf, layer, tk.MaskMode.kPrecomputed)
+    a = tk.packed_gemm(buf, layer, tk.MaskMode.kOnTheFly).cpu().numpy()
+    layer.precompute_masks()
+    b = tk.packed_gemm(buf, layer, tk.MaskMode.kPrecomputed).cpu().numpy()
+    c = tk.packed_gemm(buf, layer, tk.MaskMode.kOnTheFly, workers=3).cpu().numpy()
+    assert np.array_equal(a, b) and np.array_equal(a, c)
+    wrows, ws = oracle.pack_rows(wq)
+    assert np.array_equal(a, oracle.packed_gemm(u64(buf.words), wrows, ws, 1))
+    # all-zero weights -> zero gemm (R:tests/test_linalg.cpp:233-242)
+    z = _layer(tk, np.zeros((3, 8), np.int8), 8, 3, 1, 1, 0, ta=(0.5, 0.5))
+    bz = tk.im2col_quantize_pack(x[:32], tk.TensorShape(4, 8, 1, 1), tk.QuantThresholds(0.5, 0.5), z.geom,
+                                 tk.QuantMode.kActivationNonneg)
+    assert not tk.packed_gemm(bz, z).cpu().numpy().any()
+    with pytest.raises(tk.InvalidArgument):
+        tk.make_packed_conv_layer(np.zeros(7, np.int8), tk.ConvGeometry(4, 2, 1, 1, 1, 0),
+                                  tk.QuantThresholds(), tk.QuantThresholds(), True)
+
+
+def test_selector_row(tk):
+    """R:tests/test_linalg.cpp:177-190."""
+    n = 40
+    w = np.zeros(n, np.int8)
+    w[0] = 1
+    layer = _layer(tk, w, n, 1, 1, 1, 0, ta=(1, 1), nonneg=False)
+    x = np.random.default_rng(35).standard_normal(6 * n).astype(np.float32)
+    buf = tk.im2col_quantize_pack(x, tk.TensorShape(6, n, 1, 1), tk.QuantThresholds(1, 1), layer.geom,
+                                  tk.QuantMode.kWeight)
+    out = tk.packed_gemm(buf, layer).cpu().numpy().reshape(-1)
+    want = [(1 if v > 0.5 else (-1 if v < -0.5 else 0)) for v in x[::n]]
+    assert list(out) == want
+
+
+@pytest.mark.parametrize("backend", ["POPC", "TC_I8"])
+def test_conv_properties(tk, oracle, backend):
+    """Batch independence (exact), out_scale linearity, geometry grid, zero-input FC
+    (R:tests/test_linalg.cpp:267-380)."""
+    rng = np.random.default_rng(45)
+    TS = tk.TensorShape
+    wq = rng.integers(-1, 2, (5, 27)).astype(np.int8)
+    layer = _layer(tk, wq, 3, 5, 3, 1, 1, ta=(0.5, 0.5))
+    layer.set_backend(tk.Backend[backend])
+    xa = np.abs(rng.standard_normal(108)).astype(np.float32)
+    xb = np.abs(rng.standard_normal(108)).astype(np.float32)
+    ra = tk.conv2d_ternary(xa, TS(1, 3, 6, 6), layer).data.cpu().numpy()
+    rb = tk.conv2d_ternary(xb, TS(1, 3, 6, 6), layer).data.cpu().numpy()
+    rc = tk.conv2d_ternary(np.concatenate([xa, xb]), TS(2, 3, 6, 6), layer).data.cpu().numpy()
+    assert np.array_equal(rc, np.concatenate([ra, rb]))
+    l3 = _layer(tk, wq, 3, 5, 3, 1, 1, ta=(0.5, 0.5), out_scale=3.0)
+    l3.set_backend(tk.Backend[backend])
+    r3 = tk.conv2d_ternary(xa, TS(1, 3, 6, 6), l3).data.cpu().numpy()
+    np.testing.assert_allclose(r3, 3.0 * ra, rtol=1e-6)
+    for kh in (1, 3, 5):
+        for stride in (1, 2, 3):
+            for pad in (0, 1, 2):
+                if 11 + 2 * pad < kh or 9 + 2 * pad < kh:
+                    continue
+                w1 = rng.integers(-1, 2, (1, 2 * kh * kh)).astype(np.int8)
+                L = _layer(tk, w1, 2, 1, kh, stride, pad, ta=(0.5, 0.5))
+                L.set_backend(tk.Backend[backend])
+                x = np.abs(rng.standard_normal(2 * 11 * 9)).astype(np.float32)
+                r = tk.conv2d_ternary(x, TS(1, 2, 11, 9), L)
+                assert (r.shape.h, r.shape.w) == ((11 + 2 * pad - kh) // stride + 1, (9 + 2 * pad - kh) // stride + 1)
+                st, want = oracle.conv2d_ternary(x, 1, 2, 11, 9, w1, 1, kh, stride, pad, (0.5, 0.5), True)
+                assert np.array_equal(r.data.cpu().numpy(), want)
+    aff = tk.ChannelAffine(np.array([1, 2, 3], np.float32), np.array([0.5, -0.5, 4.0], np.float32))
+    fc = tk.make_packed_conv_layer(rng.integers(-1, 2, 24).astype(np.int8), tk.ConvGeometry(8, 3, 1, 1, 1, 0),
+                                   tk.QuantThresholds(), tk.QuantThresholds(0.5, 0.5), True, aff)
+    fc.set_backend(tk.Backend[backend])
+    y = tk.fully_connected_ternary(np.zeros(8, np.float32), 1, fc).cpu().numpy()
+    assert list(y[0]) == [0.5, -0.5, 4.0]
+
+
+@pytest.mark.parametrize("backend", ["POPC", "TC_I8"])
+def test_fc_golden_and_geometry(tk, golden, backend):
+    for name in ("fc_small", "fc_mid"):
+        bt, cin, cout = map(int, golden[f"{name}_dims"])
+        layer = _layer(tk, golden[f"{name}_w"], cin, cout, 1, 1, 0, gain=golden[f"{name}_gain"],
+                       bias=golden[f"{name}_bias"])
+        layer.set_backend(tk.Backend[backend])
+        y = tk.fully_connected_ternary(golden[f"{name}_x"], bt, layer).cpu().numpy()
+        assert np.array_equal(y.view(np.int32), golden[f"{name}_y"].view(np.int32)), name
+    bad = _layer(tk, np.zeros((6, 180), np.int8), 20, 6, 3, 1, 1)
+    with pytest.raises(tk.InvalidArgument):
+        tk.fully_connected_ternary(np.zeros(60, np.float32), 3, bad)
+
+
+@pytest.mark.parametrize("backend", ["POPC", "TC_I8"])
+def test_fc_cfg3_full_size(tk, oracle, backend):
+    """cfg3: FC 4096x4096, batch 256 -- exact int32 accumulators vs a numpy
+    integer matmul of the decoded levels (size-independent exactness), and the
+    fused float epilogue vs the oracle's formula on a row subsample."""
+    rng = np.random.default_rng(33)
+    B, N = 256, 4096
+    x = np.abs(rng.standard_normal((B, N))).astype(np.float32)
+    wq = rng.integers(-1, 2, (N, N)).astype(np.int8)
+    layer = _layer(tk, wq, N, N, 1, 1, 0, gain=(rng.uniform(0.5, 1.5, N) / 64).astype(np.float32),
+                   bias=rng.standard_normal(N).astype(np.float32))
+    layer.set_backend(tk.Backend[backend])
+    buf = tk.im2col_quantize_pack(x, tk.TensorShape(B, N, 1, 1), tk.QuantThresholds(0.5, 0.9), layer.geom,
+                                  tk.QuantMode.kActivationNonneg)
+    acc = tk.packed_gemm(buf, layer).cpu().numpy()
+    lv = np.stack([oracle.unpack(r, N) for r in u64(buf.words)]).astype(np.int64) + 1
+    want = lv @ wq.T.astype(np.int64)
+    assert np.array_equal(acc, want)
+    y = tk.fully_connected_ternary(x, B, layer).cpu().numpy()
+    rows = slice(0, 256, 51)  # rows are independent: oracle on a subsample
+    xs = np.ascontiguousarray(x[rows])
+    st, ref = oracle.conv2d_ternary(xs, xs.shape[0], N, 1, 1, wq, N, 1, 1, 0, (0.5, 0.9), True,
+                                    layer.fused.gain, layer.fused.bias, 1.0)
+    assert st == 0
+    assert np.array_equal(y[rows].view(np.int32), ref.reshape(xs.shape[0], N).view(np.int32))
