@@ -143,6 +143,20 @@ int tk_conv2d_ternary(tk_context* ctx, const tk_layer* layer, const float* x,
                       int n, int h, int w, int mask_mode, float* out,
                       void* stream);
 
+/* Ternary GEMM on operands already expanded to quantization levels (s8,
+ * [m_rows][layer k_pad], zero-padded past the patch length): the contraction
+ * packed_gemm performs, without the pack/expand step.  out_mode 0: int32
+ * [m_rows][out_c] accumulators; 1: f32 rows after the folded-BN epilogue.
+ * Uses the layer's backend choice (tensor cores for TC_I8/AUTO). */
+int tk_gemm_levels(tk_context* ctx, const tk_layer* layer, const int8_t* a_s8,
+                   int m_rows, int out_mode, void* out, void* stream);
+/* Quantize f32 rows to s8 levels for tk_gemm_levels (activation levels
+ * {0,1,2} in nonneg mode, {-1,0,1} in weight mode), zero padded to k_pad. */
+int tk_quantize_levels(tk_context* ctx, const float* x, int rows, int n,
+                       float alpha1, float alpha2, int mode, int k_pad,
+                       int8_t* out, void* stream);
+int tk_layer_k_pad(const tk_layer* layer);
+
 /* fully_connected_ternary(x, batch, layer, mask_mode) R:linalg.hpp:332-343 */
 int tk_fully_connected_ternary(tk_context* ctx, const tk_layer* layer,
                                const float* x, int batch, int mask_mode,

@@ -59,6 +59,9 @@ SIGNATURES = {
     "tk_packed_gemm": (_i, [_vp, _vp, _vp, _sz, _sz, _i, _i, _vp, _vp]),
     "tk_conv2d_ternary": (_i, [_vp, _vp, _vp, _i, _i, _i, _i, _vp, _vp]),
     "tk_fully_connected_ternary": (_i, [_vp, _vp, _vp, _i, _i, _vp, _vp]),
+    "tk_gemm_levels": (_i, [_vp, _vp, _vp, _i, _i, _vp, _vp]),
+    "tk_quantize_levels": (_i, [_vp, _vp, _i, _i, _f, _f, _i, _i, _vp, _vp]),
+    "tk_layer_k_pad": (_i, [_vp]),
 }
 
 _lib = None

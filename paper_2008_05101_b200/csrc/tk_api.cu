@@ -417,6 +417,29 @@ int tk_conv2d_ternary(tk_context* ctx, const tk_layer* L, const float* x,
   return TK_OK;
 }
 
+int tk_layer_k_pad(const tk_layer* L) { return L ? L->k_pad : -1; }
+
+int tk_gemm_levels(tk_context* ctx, const tk_layer* L, const int8_t* a_s8, int m_rows,
+                   int out_mode, void* out, void* stream) {
+  if (!ctx || !L || m_rows < 0 || (out_mode != 0 && out_mode != 1)) return TK_ERR_INVALID;
+  if (m_rows == 0) return TK_OK;
+  if (!tk_tc_supported(m_rows, L->out_c, L->k_pad)) return TK_ERR_UNSUPPORTED;
+  tk_epilogue e{out_mode == 0 ? TK_EPI_I32 : TK_EPI_F32_ROWS, 1, L->d_gain, L->d_bias,
+                L->out_scale, out};
+  TK_CUDA(tk_launch_gemm_tc(a_s8, m_rows, L->k_pad, L, e, (cudaStream_t)stream));
+  return TK_OK;
+}
+
+int tk_quantize_levels(tk_context* ctx, const float* x, int rows, int n, float a1, float a2,
+                       int mode, int k_pad, int8_t* out, void* stream) {
+  if (!ctx || rows < 0 || n < 0 || k_pad < n || k_pad % 16) return TK_ERR_INVALID;
+  tk_qparams q;
+  const int st = tk_make_qparams(a1, a2, mode, &q);
+  if (st != TK_OK) return st;
+  TK_CUDA(tk_launch_quantize_s8(x, rows, n, q, k_pad, out, ctx->d_err, (cudaStream_t)stream));
+  return TK_OK;
+}
+
 // R:linalg.hpp:332-343: a 1x1, pad-0 conv over [batch][in_c][1][1]
 int tk_fully_connected_ternary(tk_context* ctx, const tk_layer* L,
                                const float* x, int batch, int mask_mode,

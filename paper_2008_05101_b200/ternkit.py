@@ -495,3 +495,33 @@ def fully_connected_ternary(x, batch: int, layer: PackedConvLayer,
     if check_errors:
         sync("fully_connected_ternary")
     return out
+
+
+# ---------------------------------------------------------------------------
+# level-operand entry points (tensor-core path without the 2-bit pack step)
+
+
+def quantize_levels(x, t: QuantThresholds, mode: QuantMode, k_pad: int) -> torch.Tensor:
+    """f32 [rows][n] -> s8 quantization levels [rows][k_pad] (zero padded)."""
+    xd = _dev(x, torch.float32)
+    rows, n = xd.shape
+    out = torch.empty((rows, k_pad), dtype=torch.int8, device="cuda")
+    check(T.lib().tk_quantize_levels(context(), _p(xd), rows, n, t.alpha1, t.alpha2, int(mode), k_pad,
+                                     _p(out), _stream()), "quantize_levels")
+    return out
+
+
+def gemm_levels(a_s8: torch.Tensor, layer: PackedConvLayer, fused: bool = False,
+                out: torch.Tensor | None = None) -> torch.Tensor:
+    """Ternary GEMM on s8 level operands: int32 accumulators, or (fused=True)
+    f32 rows after the folded-BN epilogue."""
+    m = a_s8.shape[0]
+    if out is None:
+        out = torch.empty((m, layer.geom.out_c), dtype=torch.float32 if fused else torch.int32, device="cuda")
+    check(T.lib().tk_gemm_levels(context(), layer.handle, _p(a_s8), m, 1 if fused else 0, _p(out),
+                                 _stream()), "gemm_levels")
+    return out
+
+
+def layer_k_pad(layer: PackedConvLayer) -> int:
+    return T.lib().tk_layer_k_pad(layer.handle)
