@@ -20,7 +20,6 @@
 namespace {
 
 constexpr int BM = 128, BK = 128;
-constexpr int kStages = 4;
 constexpr int kThreads = 192;
 
 template <int BN>
@@ -28,6 +27,8 @@ struct TcSmem {
   static constexpr int kA = BM * BK;          // bytes per stage
   static constexpr int kB = BN * BK;
   static constexpr int kStage = kA + kB;
+  // as many stages as ~200 KB of shared memory holds (latency hiding)
+  static constexpr int kStages = (200 * 1024 / kStage) > 8 ? 8 : (200 * 1024 / kStage);
   static constexpr int kBytes = kStages * kStage + 1024 /*align*/ + 256 /*barriers*/;
 };
 
@@ -35,11 +36,12 @@ template <int BN>
 __global__ void __launch_bounds__(kThreads, 1)
 k_gemm_tc_i8(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
              int M, int N, int num_kb, tk_epilogue e) {
+  constexpr int kStages = TcSmem<BN>::kStages;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
-  uint8_t* sB = smem + kStages * TcSmem<BN>::kA;
+  uint8_t* sB = smem + kStages * TcSmem<BN>::kA;  // A ring, then B ring
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * TcSmem<BN>::kStage);
   uint64_t* empty = full + kStages;
   uint64_t* tmem_full = empty + kStages;
@@ -67,12 +69,17 @@ k_gemm_tc_i8(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
 
   if (warp == 0 && lane == 0) {
     // ---- TMA producer ----
+    // CTAs sharing an A tile start at different K blocks (integer sums are
+    // order independent) so they do not hammer the same L2 lines at once
+    const int k_rot = blockIdx.x % num_kb;
     for (int kb = 0; kb < num_kb; ++kb) {
       const int s = kb % kStages;
       if (kb >= kStages) sm100::mbar_wait(&empty[s], ((kb / kStages) - 1) & 1);
+      int kk = kb + k_rot;
+      if (kk >= num_kb) kk -= num_kb;
       sm100::mbar_arrive_expect_tx(&full[s], TcSmem<BN>::kStage);
-      sm100::tma_load_2d(sA + s * TcSmem<BN>::kA, &tmA, &full[s], kb * BK, m0);
-      sm100::tma_load_2d(sB + s * TcSmem<BN>::kB, &tmB, &full[s], kb * BK, n0);
+      sm100::tma_load_2d(sA + s * TcSmem<BN>::kA, &tmA, &full[s], kk * BK, m0);
+      sm100::tma_load_2d(sB + s * TcSmem<BN>::kB, &tmB, &full[s], kk * BK, n0);
     }
   } else if (warp == 1 && lane == 0) {
     // ---- MMA issuer: 4 x (128 x BN x 32) per stage ----
