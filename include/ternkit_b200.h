@@ -162,6 +162,49 @@ int tk_fully_connected_ternary(tk_context* ctx, const tk_layer* layer,
                                const float* x, int batch, int mask_mode,
                                float* out, void* stream);
 
+/* ---- network-level packed inference (R:tinynet.hpp:713-735 pattern) -------
+ * A body is a sequence of residual blocks of conv2d_ternary layers (folded BN
+ * in each layer's affine): inner convs are followed by ReLU; the last conv's
+ * output is added to the shortcut (identity, or a 1x1 downsample conv) and
+ * ReLU'd -- exactly the reference composition z = max(z + id, 0)
+ * (R:tinynet.hpp:720-730) applied to conv layers.  Layout of the structs
+ * matches oracle/netdesc.h. */
+typedef struct {
+  int in_c, out_c, k, stride, pad;
+  const int8_t* weights_host; /* [out_c][(ky*k + kx)*in_c + c] in {-1,0,1} */
+  float tw1, tw2, ta1, ta2;
+  const float* gain_host;     /* folded BN, out_c (NULL = identity) */
+  const float* bias_host;
+  float out_scale;
+} tk_conv_desc;
+
+typedef struct {
+  int n_convs;                /* 2 (basic) or 3 (bottleneck) */
+  tk_conv_desc conv[3];
+  int has_down;
+  tk_conv_desc down;          /* 1x1 shortcut conv */
+} tk_block_desc;
+
+typedef struct tk_net tk_net;
+
+#define TK_NET_AUTO 0     /* fused tensor-core pipeline when the shapes allow */
+#define TK_NET_GENERIC 1  /* layer-by-layer conv2d_ternary (any shape)        */
+
+/* Builds device weights, activation buffers (batch fixed) and launch plans. */
+int tk_net_create(tk_context* ctx, const tk_block_desc* blocks, int n_blocks,
+                  int batch, int in_c, int in_h, int in_w, int mode,
+                  tk_net** out);
+int tk_net_destroy(tk_net* net);
+int tk_net_out_shape(const tk_net* net, int* c, int* h, int* w);
+/* 1 = fused tensor-core pipeline, 0 = generic layer-by-layer path */
+int tk_net_is_fused(const tk_net* net);
+/* x: [batch][in_c][in_h][in_w] f32 (device).  out (nullable): body output
+ * [batch][C][H][W] f32; pooled (nullable): its spatial mean [batch][C]. */
+int tk_net_forward(tk_context* ctx, tk_net* net, const float* x, float* out,
+                   float* pooled, void* stream);
+/* number of kernel launches one tk_net_forward issues */
+int tk_net_launches(const tk_net* net, int with_out, int with_pooled);
+
 #ifdef __cplusplus
 }
 #endif

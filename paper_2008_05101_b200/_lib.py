@@ -62,7 +62,30 @@ SIGNATURES = {
     "tk_gemm_levels": (_i, [_vp, _vp, _vp, _i, _i, _vp, _vp]),
     "tk_quantize_levels": (_i, [_vp, _vp, _i, _i, _f, _f, _i, _i, _vp, _vp]),
     "tk_layer_k_pad": (_i, [_vp]),
+    "tk_net_create": (_i, [_vp, _vp, _i, _i, _i, _i, _i, _i, C.POINTER(_vp)]),
+    "tk_net_destroy": (_i, [_vp]),
+    "tk_net_out_shape": (_i, [_vp, C.POINTER(_i), C.POINTER(_i), C.POINTER(_i)]),
+    "tk_net_is_fused": (_i, [_vp]),
+    "tk_net_forward": (_i, [_vp, _vp, _vp, _vp, _vp, _vp]),
+    "tk_net_launches": (_i, [_vp, _i, _i]),
 }
+
+TK_NET_AUTO = 0
+TK_NET_GENERIC = 1
+
+
+class ConvDesc(C.Structure):
+    """tk_conv_desc (include/ternkit_b200.h)."""
+    _fields_ = [("in_c", _i), ("out_c", _i), ("k", _i), ("stride", _i), ("pad", _i),
+                ("weights_host", C.POINTER(C.c_int8)),
+                ("tw1", _f), ("tw2", _f), ("ta1", _f), ("ta2", _f),
+                ("gain_host", C.POINTER(_f)), ("bias_host", C.POINTER(_f)),
+                ("out_scale", _f)]
+
+
+class BlockDesc(C.Structure):
+    """tk_block_desc (include/ternkit_b200.h)."""
+    _fields_ = [("n_convs", _i), ("conv", ConvDesc * 3), ("has_down", _i), ("down", ConvDesc)]
 
 _lib = None
 

@@ -1,0 +1,293 @@
+"""ResNet-18/50-shaped ternary networks on the fused B200 pipeline.
+
+The reference has no ResNet definition; these networks apply
+its network composition pattern -- packed_forward, R:tinynet.hpp:713-735 --
+to conv layers: every quantized layer is conv2d_ternary (R:linalg.hpp:301-328)
+with its folded BN, inner convs are followed by ReLU, and each block ends with
+z = max(conv(h) + shortcut, 0).  As in the paper's protocol
+the first (7x7 stem) and last (FC head) layers stay in float.
+
+    TernaryBody      -- the ternary hot path (tk_net_* C-ABI, CUDA)
+    TernaryResNet    -- float stem (cuDNN) + TernaryBody + float head
+    resnet_spec()    -- synthetic random-weight ResNet-18 / ResNet-50 bodies
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import os
+
+import numpy as np
+import torch
+
+from . import _lib as T
+from ._lib import check
+from . import ternkit as tk
+
+
+# ---------------------------------------------------------------------------
+# synthetic specs
+
+def _conv(rng, in_c, out_c, k, stride, ta, relu_follows=True):
+    K = in_c * k * k
+    # folded BN: gain normalises the ternary accumulator to ~unit variance
+    # (E[a^2] ~ 1.8 for levels of half-normal inputs, E[w^2] = 2/3) so every
+    # quantization level keeps occurring layer after layer.
+    gain = (rng.uniform(0.8, 1.2, out_c) / math.sqrt(K * 1.2)).astype(np.float32)
+    bias = (rng.standard_normal(out_c) * 0.25 - (0.0 if relu_follows else 0.3)).astype(np.float32)
+    return dict(in_c=in_c, out_c=out_c, k=k, stride=stride, pad=k // 2,
+                weights=rng.integers(-1, 2, (out_c, K)).astype(np.int8),
+                ta=ta, tw=(1.0, 1.0), gain=gain, bias=bias, out_scale=1.0)
+
+
+def resnet_spec(depth: int = 18, seed: int = 0, width: int = 64):
+    """Body blocks (after the stem, input width x 56 x 56) of a ResNet-depth."""
+    rng = np.random.default_rng(seed)
+    blocks = []
+    c = width
+    ta = lambda: (float(np.float32(rng.uniform(0.4, 0.6))), float(np.float32(rng.uniform(0.8, 1.0))))  # noqa: E731
+    if depth == 18:
+        for stage, (w, n) in enumerate([(64, 2), (128, 2), (256, 2), (512, 2)]):
+            for i in range(n):
+                s = 2 if (stage > 0 and i == 0) else 1
+                t1 = ta()
+                blk = dict(convs=[_conv(rng, c, w, 3, s, t1), _conv(rng, w, w, 3, 1, ta(), False)])
+                if s != 1 or c != w:
+                    blk["down"] = _conv(rng, c, w, 1, s, t1, False)
+                blocks.append(blk)
+                c = w
+    elif depth == 50:
+        for stage, (w, n) in enumerate([(64, 3), (128, 4), (256, 6), (512, 3)]):
+            for i in range(n):
+                s = 2 if (stage > 0 and i == 0) else 1
+                t1 = ta()
+                blk = dict(convs=[_conv(rng, c, w, 1, s, t1), _conv(rng, w, w, 3, 1, ta()),
+                                  _conv(rng, w, 4 * w, 1, 1, ta(), False)])
+                if s != 1 or c != 4 * w:
+                    blk["down"] = _conv(rng, c, 4 * w, 1, s, t1, False)
+                blocks.append(blk)
+                c = 4 * w
+    else:
+        raise ValueError("depth must be 18 or 50")
+    return blocks
+
+
+def body_macs(blocks, h=56, w=56) -> int:
+    """Ternary multiply-accumulates per image of a body spec."""
+    macs = 0
+    for blk in blocks:
+        hh, ww = h, w
+        for cv in blk["convs"]:
+            hh = (hh + 2 * cv["pad"] - cv["k"]) // cv["stride"] + 1
+            ww = (ww + 2 * cv["pad"] - cv["k"]) // cv["stride"] + 1
+            macs += hh * ww * cv["out_c"] * cv["in_c"] * cv["k"] ** 2
+        if blk.get("down") is not None:
+            d = blk["down"]
+            macs += hh * ww * d["out_c"] * d["in_c"]
+        h, w = hh, ww
+    return macs
+
+
+# ---------------------------------------------------------------------------
+# the ternary body on the GPU
+
+def _desc(cv, keep) -> T.ConvDesc:
+    w = np.ascontiguousarray(cv["weights"], dtype=np.int8)
+    g = np.ascontiguousarray(cv["gain"], dtype=np.float32)
+    b = np.ascontiguousarray(cv["bias"], dtype=np.float32)
+    keep += [w, g, b]
+    tw = cv.get("tw", (1.0, 1.0))
+    return T.ConvDesc(cv["in_c"], cv["out_c"], cv["k"], cv["stride"], cv["pad"],
+                      w.ctypes.data_as(C.POINTER(C.c_int8)), tw[0], tw[1], cv["ta"][0], cv["ta"][1],
+                      g.ctypes.data_as(C.POINTER(C.c_float)), b.ctypes.data_as(C.POINTER(C.c_float)),
+                      cv.get("out_scale", 1.0))
+
+
+class TernaryBody:
+    """Residual ternary conv body (tk_net).  forward(x) takes the body input
+    [batch][C][H][W] f32 on the device; returns pooled [batch][C'] and, if
+    asked, the full [batch][C'][H'][W'] output."""
+
+    def __init__(self, blocks, batch: int, in_c: int, in_h: int, in_w: int,
+                 mode: int = T.TK_NET_AUTO):
+        self.blocks = blocks
+        self.batch, self.in_c, self.in_h, self.in_w = batch, in_c, in_h, in_w
+        keep: list = []
+        arr = (T.BlockDesc * len(blocks))()
+        for i, blk in enumerate(blocks):
+            arr[i].n_convs = len(blk["convs"])
+            for j, cv in enumerate(blk["convs"]):
+                arr[i].conv[j] = _desc(cv, keep)
+            if blk.get("down") is not None:
+                arr[i].has_down = 1
+                arr[i].down = _desc(blk["down"], keep)
+        h = C.c_void_p()
+        check(T.lib().tk_net_create(tk.context(), C.cast(arr, C.c_void_p), len(blocks), batch, in_c,
+                                    in_h, in_w, mode, C.byref(h)), "tk_net_create")
+        self._h = h.value
+        oc, oh, ow = C.c_int(), C.c_int(), C.c_int()
+        check(T.lib().tk_net_out_shape(self._h, C.byref(oc), C.byref(oh), C.byref(ow)), "out_shape")
+        self.out_shape = (oc.value, oh.value, ow.value)
+        self.fused = bool(T.lib().tk_net_is_fused(self._h))
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            try:
+                T.lib().tk_net_destroy(self._h)
+            except Exception:
+                pass
+            self._h = None
+
+    def launches(self, with_out=False, with_pooled=True) -> int:
+        return T.lib().tk_net_launches(self._h, int(with_out), int(with_pooled))
+
+    def forward(self, x: torch.Tensor, want_out: bool = False, pooled: torch.Tensor | None = None,
+                out: torch.Tensor | None = None, check_errors: bool = True):
+        assert x.is_cuda and x.dtype == torch.float32 and x.is_contiguous()
+        assert x.numel() == self.batch * self.in_c * self.in_h * self.in_w
+        c, h, w = self.out_shape
+        if pooled is None:
+            pooled = torch.empty((self.batch, c), dtype=torch.float32, device="cuda")
+        if want_out and out is None:
+            out = torch.empty((self.batch, c, h, w), dtype=torch.float32, device="cuda")
+        check(T.lib().tk_net_forward(tk.context(), self._h, x.data_ptr(),
+                                     out.data_ptr() if want_out else None, pooled.data_ptr(),
+                                     tk._stream()), "tk_net_forward")
+        if check_errors:
+            tk.sync("tk_net_forward")
+        return (pooled, out) if want_out else pooled
+
+
+class TernaryResNet:
+    """Float stem + ternary body + float head, images [batch][3][224][224]."""
+
+    def __init__(self, depth: int = 18, batch: int = 256, seed: int = 0, classes: int = 1000):
+        g = torch.Generator().manual_seed(seed)
+        self.batch = batch
+        self.stem_w = (torch.randn(64, 3, 7, 7, generator=g) / math.sqrt(3 * 49)).cuda()
+        self.stem_gain = (torch.rand(64, generator=g) * 0.5 + 0.75).cuda()
+        self.stem_bias = (torch.randn(64, generator=g) * 0.1).cuda()
+        self.blocks = resnet_spec(depth, seed)
+        self.body = TernaryBody(self.blocks, batch, 64, 56, 56)
+        c = self.body.out_shape[0]
+        self.head_w = (torch.randn(classes, c, generator=g) / math.sqrt(c)).cuda()
+        self.head_b = torch.zeros(classes).cuda()
+
+    def stem(self, images: torch.Tensor) -> torch.Tensor:
+        with torch.backends.cudnn.flags(enabled=True, allow_tf32=False):
+            y = torch.nn.functional.conv2d(images, self.stem_w, stride=2, padding=3)
+        y = torch.relu(y * self.stem_gain.view(1, -1, 1, 1) + self.stem_bias.view(1, -1, 1, 1))
+        return torch.nn.functional.max_pool2d(y, 3, 2, 1).contiguous()
+
+    def forward(self, images: torch.Tensor, check_errors: bool = False) -> torch.Tensor:
+        x = self.stem(images)
+        pooled = self.body.forward(x, check_errors=check_errors)
+        return torch.addmm(self.head_b, pooled, self.head_w.t(), beta=1.0, alpha=1.0)
+
+
+# ---------------------------------------------------------------------------
+# bench workload (cfg4 ResNet-18 b256 / cfg5 ResNet-50)
+
+class ResNetWorkload:
+    """One step = the ternary body on one batch resident in HBM (the paper's
+    protocol: first and last layers excluded); e2e = the whole network from
+    host images (pinned H2D) to logits (D2H)."""
+
+    def __init__(self, name: str = "resnet18", batch: int | None = None, seed: int = 0):
+        depth = 18 if name == "resnet18" else 50
+        batch = batch or int(os.environ.get("TK_BENCH_BATCH", 256 if depth == 18 else 128))
+        self.name, self.depth, self.B = name, depth, batch
+        self.net = TernaryResNet(depth, batch, seed)
+        g = torch.Generator().manual_seed(seed + 1)
+        self.images_host = torch.rand(batch, 3, 224, 224, generator=g).pin_memory()
+        self.images_dev = self.images_host.cuda()
+        self.x = self.net.stem(self.images_dev)  # body input, resident
+        self.pooled = torch.empty((batch, self.net.body.out_shape[0]), device="cuda")
+        self.logits_host = torch.empty((batch, 1000)).pin_memory()
+        self.img_dev2 = torch.empty_like(self.images_dev)
+        self.macs_per_img = body_macs(self.net.blocks)
+        self.units_per_step = float(batch)
+        self.unit = "img/s"
+        self.launches_per_step = self.net.body.launches(False, True)
+        self.config = {"workload": f"cfg{'4' if depth == 18 else '5'} {name} ternary body, synthetic 224x224 "
+                                   f"images, batch {batch} per GPU (paper protocol: float stem/head excluded "
+                                   f"from value, included in e2e)",
+                       "model": name, "batch_per_gpu": batch, "image": 224,
+                       "fused_pipeline": self.net.body.fused,
+                       "body_gmac_per_img": round(self.macs_per_img / 1e9, 4),
+                       "l2": "flushed between steps (256 MB write)"}
+
+    def step(self):
+        return self.net.body.forward(self.x, pooled=self.pooled, check_errors=False)
+
+    def step_e2e(self):
+        self.img_dev2.copy_(self.images_host, non_blocking=True)
+        logits = self.net.forward(self.img_dev2)
+        self.logits_host.copy_(logits, non_blocking=True)
+        return logits
+
+    def e2e_bytes(self):
+        return self.images_host.numel() * 4, self.B * 1000 * 4
+
+    def dominant(self):
+        """Dominant kernel: the whole ternary body (its convs are >95% of the
+        step); algorithmic work = 2 x body MACs."""
+        flops = 2.0 * self.macs_per_img * self.B
+        return ("ternary conv body (tcgen05 kind::i8 fused convs)" if self.net.body.fused else
+                "ternary conv body (generic)", flops / 1e12, "TFLOP/s", "tensor", self.step, None)
+
+    def verify(self) -> bool:
+        """Body parity on a 2-image subsample vs the C oracle (bit-exact f32)."""
+        from oracle.oracle import Oracle
+        O = Oracle()
+        sub = 2
+        xb = self.x[:sub].contiguous()
+        body2 = TernaryBody(self.net.blocks, sub, 64, 56, 56)
+        _, out = body2.forward(xb, want_out=True)
+        st, want = O.net_body(self.net.blocks, xb.cpu().numpy(), sub, 64, 56, 56)
+        return st == 0 and np.array_equal(out.cpu().numpy().view(np.int32), want.view(np.int32))
+
+    def cpu_baseline(self, threads: int) -> dict:
+        from oracle.oracle import Reference
+        R = Reference()
+        n = threads
+        xs = np.ascontiguousarray(self.x[:n].cpu().numpy())
+        h = R.net_create(self.net.blocks)
+        st, _, sec = R.net_run(h, xs, n, 64, 56, 56, threads)
+        R.net_destroy(h)
+        assert st == 0
+        return {"value": n / sec, "unit": "img/s", "cores": threads, "kind": "reference",
+                "sample": f"{n} images of the batch, one per host thread, reference conv2d_ternary "
+                          f"composition (oracle/_ref, unmodified headers)", "seconds": sec}
+
+
+def reference_cpu_run(args, metric: str, threads: int) -> dict:
+    """bench.py --impl reference for the ResNet workloads: the reference's own
+    CPU implementation (oracle/_ref) of the ternary body, all host threads,
+    each step a bounded sample of `threads` images."""
+    import statistics
+    from oracle.oracle import Reference
+    depth = 18 if args.workload == "resnet18" else 50
+    blocks = resnet_spec(depth, 0)
+    R = Reference()
+    h = R.net_create(blocks)
+    rng = np.random.default_rng(1)
+    n = threads
+    x = np.maximum(rng.standard_normal((n, 64, 56, 56)), 0).astype(np.float32)
+    vals = []
+    for i in range(args.warmup + args.steps):
+        st, _, sec = R.net_run(h, x, n, 64, 56, 56, threads)
+        assert st == 0
+        if i >= args.warmup:
+            vals.append(n / sec)
+    R.net_destroy(h)
+    v = statistics.mean(vals)
+    batch = 256 if depth == 18 else 128
+    cb = {"value": round(v, 4), "unit": "img/s", "cores": threads, "kind": "reference",
+          "sample": f"{n} images per step (one per host thread) of the batch-{batch} workload"}
+    return {"metric": metric, "impl": "reference", "value": round(v, 4), "unit": "img/s", "n_gpus": 0,
+            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+            "config": {"workload": f"{args.workload} ternary body (reference CPU, oracle/_ref)",
+                       "model": args.workload, "batch_per_gpu": batch},
+            "cpu_baseline": cb,
+            "e2e": {"value": round(v, 4), "unit": "img/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}

@@ -1,0 +1,115 @@
+"""GPU parity of network-level inference: the fused tensor-core conv pipeline
+and the generic layer-by-layer path vs the C oracle's restatement of the
+reference composition (which tests/test_oracle_golden.py pins to the compiled
+reference).  Body outputs are compared bit-exactly as f32 -- the integer
+accumulators, folded-BN FMA, skip add, ReLU and every intermediate
+quantization must all agree for that to hold."""
+import numpy as np
+import pytest
+import torch
+
+from tests.netspec import conv_spec, tiny_body
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(blocks, x, n, c, h, w, mode=0):
+    from paper_2008_05101_b200.resnet import TernaryBody
+    body = TernaryBody(blocks, n, c, h, w, mode=mode)
+    pooled, out = body.forward(torch.from_numpy(x.reshape(n, c, h, w)).cuda(), want_out=True)
+    return body, pooled.cpu().numpy(), out.cpu().numpy()
+
+
+def _check(oracle, blocks, x, n, c, h, w, expect_fused):
+    body, pooled, out = _run(blocks, x, n, c, h, w)
+    assert body.fused == expect_fused
+    st, want = oracle.net_body(blocks, x, n, c, h, w)
+    assert st == 0
+    assert out.shape == want.shape
+    mism = np.count_nonzero(out.view(np.int32) != want.view(np.int32))
+    assert mism == 0, f"{mism} of {out.size} body outputs differ"
+    np.testing.assert_allclose(pooled, want.reshape(n, want.shape[1], -1).mean(-1), rtol=1e-5, atol=1e-5)
+    assert (want > 0).mean() > 0.1
+    return body, out
+
+
+def test_generic_path_tiny_body(oracle):
+    blocks, (n, c, h, w), x = tiny_body(seed=3)
+    _check(oracle, blocks, x, n, c, h, w, expect_fused=False)
+
+
+def fused_small(seed=0, n=3, h=16, w=16):
+    rng = np.random.default_rng(seed)
+    blocks = [
+        dict(convs=[conv_spec(rng, 64, 64, 3, 1, 1), conv_spec(rng, 64, 64, 3, 1, 1, (0.45, 0.8))]),
+        dict(convs=[conv_spec(rng, 64, 128, 3, 2, 1), conv_spec(rng, 128, 128, 3, 1, 1)],
+             down=conv_spec(rng, 64, 128, 1, 2, 0)),
+        dict(convs=[conv_spec(rng, 128, 64, 1, 1, 0), conv_spec(rng, 64, 64, 3, 1, 1, (0.4, 0.7)),
+                    conv_spec(rng, 64, 128, 1, 1, 0)]),
+        dict(convs=[conv_spec(rng, 128, 128, 1, 2, 0), conv_spec(rng, 128, 128, 3, 1, 1),
+                    conv_spec(rng, 128, 256, 1, 1, 0)],
+             down=conv_spec(rng, 128, 256, 1, 2, 0, (0.6, 1.0))),
+        dict(convs=[conv_spec(rng, 256, 512, 3, 1, 1), conv_spec(rng, 512, 256, 3, 1, 1)]),
+    ]
+    x = np.abs(rng.standard_normal(n * 64 * h * w)).astype(np.float32)
+    return blocks, (n, 64, h, w), x
+
+
+def test_fused_path_small_body(oracle):
+    """Basic, strided-with-downsample and bottleneck blocks (incl. a stride-2
+    1x1, a 512-channel conv split over two N tiles and a downsample whose
+    quantizer differs from its sibling conv's) through the fused kernels."""
+    blocks, (n, c, h, w), x = fused_small()
+    _check(oracle, blocks, x, n, c, h, w, expect_fused=True)
+
+
+def test_fused_equals_generic(oracle):
+    from paper_2008_05101_b200 import _lib as T
+    blocks, (n, c, h, w), x = fused_small(seed=5, n=2, h=12, w=20)
+    _, _, fused = _run(blocks, x, n, c, h, w, mode=T.TK_NET_AUTO)
+    _, _, generic = _run(blocks, x, n, c, h, w, mode=T.TK_NET_GENERIC)
+    assert np.array_equal(fused.view(np.int32), generic.view(np.int32))
+
+
+def test_resnet18_body_subsample(oracle):
+    """cfg4 network at full resolution (56x56 body input, 8 blocks), 2 images."""
+    from paper_2008_05101_b200.resnet import resnet_spec
+    blocks = resnet_spec(18, seed=0)
+    rng = np.random.default_rng(1)
+    x = np.maximum(rng.standard_normal(2 * 64 * 56 * 56), 0).astype(np.float32)
+    _check(oracle, blocks, x, 2, 64, 56, 56, expect_fused=True)
+
+
+def test_resnet50_body_subsample(oracle):
+    """cfg5 network (16 bottleneck blocks), 1 image."""
+    from paper_2008_05101_b200.resnet import resnet_spec
+    blocks = resnet_spec(50, seed=0)
+    rng = np.random.default_rng(2)
+    x = np.maximum(rng.standard_normal(64 * 56 * 56), 0).astype(np.float32)
+    _check(oracle, blocks, x, 1, 64, 56, 56, expect_fused=True)
+
+
+def test_batch_independence_large_batch():
+    """Images are independent: image i of a batch-64 run equals a batch-1 run."""
+    from paper_2008_05101_b200.resnet import resnet_spec
+    blocks = resnet_spec(18, seed=4)
+    rng = np.random.default_rng(3)
+    x = np.maximum(rng.standard_normal(64 * 64 * 56 * 56), 0).astype(np.float32)
+    _, _, big = _run(blocks, x, 64, 64, 56, 56)
+    for i in (0, 37, 63):
+        _, _, one = _run(blocks, x.reshape(64, -1)[i].copy(), 1, 64, 56, 56)
+        assert np.array_equal(big[i].view(np.int32), one[0].view(np.int32))
+
+
+def test_net_errors(tk):
+    from paper_2008_05101_b200.resnet import TernaryBody
+    blocks, (n, c, h, w), x = fused_small(n=1)
+    body = TernaryBody(blocks, n, c, h, w)
+    xb = torch.from_numpy(x.reshape(n, c, h, w).copy()).cuda()
+    xb[0, 5, 3, 3] = -1.0  # negative activation: R:quantizer.hpp:53-55
+    with pytest.raises(tk.InvalidArgument):
+        body.forward(xb)
+    bad = [dict(convs=[conv_spec(np.random.default_rng(0), 64, 64, 3, 1, 1),
+                       conv_spec(np.random.default_rng(0), 64, 32, 3, 1, 1)])]  # identity shape mismatch
+    with pytest.raises(tk.InvalidArgument):
+        TernaryBody(bad, 1, 64, 8, 8)
