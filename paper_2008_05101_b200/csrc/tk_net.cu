@@ -7,20 +7,24 @@
 //   h = x; for inner convs: h = max(conv2d_ternary(h), 0)
 //   out = max(conv2d_ternary_last(h) + (down ? conv2d_ternary_down(x) : x), 0)
 //
-// Fused-path data layout (all HBM-resident, per activation tensor):
+// Fused-path data layout (HBM-resident, per activation tensor):
 //  * s8 levels  [C/R][phase][pos][R]   R = 64 (C == 64) or 128 channels,
 //    pos = padded position n*PH*PW + py*PW + px of a zero-padded (pad 1)
 //    image; stride-2 consumers get the 4 (row, col)-parity phase planes so
 //    every kernel tap is a contiguous row range.  The pad ring is zero
 //    (= the code of quantize(0.0)), written once and never touched.
-//  * f32 values [C/32][pos][32] (only where a residual add needs them).
+//  * f32 NCHW tensors only where a residual add (or the head) needs floats.
 // Conv kernel (tcgen05 kind::i8): a CTA owns a 128-position tile; for each
 // 64/128-channel chunk ONE TMA box loads the tile plus halo (rows shifted by
 // up to 2*Wp+2) into SMEM with the hardware swizzle, and every tap of the
 // 3x3 window is an MMA whose A descriptor simply starts `shift` rows later
 // (verified on B200: tools/desc_test.cu).  Weights stream through a TMA ring
-// (or stay resident when they fit).  Accumulators double-buffer in TMEM so
-// the epilogue of tile i overlaps the MMAs of tile i+1.
+// (or stay resident when they fit).  Accumulators rotate through 2-4 TMEM
+// buffers so the epilogue of tile i overlaps the MMAs of the next tiles.
+// Epilogue: inner convs (ReLU then quantize for the next conv, no float
+// needed) compare the INTEGER accumulator against per-channel integer
+// thresholds precomputed from the exact float epilogue (monotone in acc), so
+// the level bytes are bit-identical to quantize(max(fma(g, s*acc, b), 0)).
 #include <cuda.h>
 #include <math.h>
 #include <stdlib.h>
@@ -35,7 +39,8 @@
 
 namespace {
 
-constexpr int kConvThreads = 192;  // warp0 TMA, warp1 MMA, warps 2-5 epilogue
+constexpr int kConvThreads = 320;  // warp0 TMA, warp1 MMA, warps 2-9 epilogue
+constexpr int kEpiThreads = 256;
 
 struct ConvK {
   int n_taps;
@@ -56,12 +61,12 @@ struct ConvK {
   // epilogue
   const float* gain;
   const float* bias;
+  const int* ithr;  // [n_q][3][N] (c0, c1, sign) integer-threshold mode, or null
   float out_scale;
   int relu;
   int N;
-  const float* skip;
-  float* fout;
-  long long f_pos;
+  const float* skip;  // NCHW
+  float* fout;        // NCHW
   int o_Hp, o_Wp, o_PH, o_PW;
   int n_q;
   int8_t* q[2];
@@ -69,6 +74,7 @@ struct ConvK {
   int q_phases[2], q_R[2];
   long long q_pos[2];
   unsigned long long* err;
+  int dbg;  // profiling knob (env TK_CONV_DBG): 1 no MMA, 2 no halo TMA, 4 no epilogue
 };
 
 __device__ __forceinline__ uint64_t desc_sw(uint32_t saddr, int R) {
@@ -81,10 +87,36 @@ __device__ __forceinline__ uint64_t desc_sw(uint32_t saddr, int R) {
   return d;
 }
 
-template <int BN, int R>
+__device__ __forceinline__ void epi_bar() {
+  asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
+}
+
+// profiling stamps (dbg & 16): per CTA [start, setup done, MMA loop done,
+// epilogue loop done, end] in globaltimer ns
+__device__ unsigned long long g_stamps[148 * 8];
+// CTA 0 event trace (dbg & 16): [role][item] for the first 32 items
+// role 0 producer after h_empty wait, 1 MMA after a_empty wait, 2 MMA after
+// h_full wait, 3 epilogue group after a_full wait, 4 epilogue done
+__device__ unsigned long long g_trace[5 * 32];
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+template <int BN>
+struct Acc {
+  static constexpr int kN = BN <= 128 ? 4 : 2;  // accumulator buffers
+  static constexpr uint32_t kCols = kN * BN;    // TMEM columns (power of 2)
+};
+
+template <int BN, int R, int KT>
 __global__ void __launch_bounds__(kConvThreads, 1)
 k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CUtensorMap w_map,
           const ConvK p) {
+  constexpr int kAcc = Acc<BN>::kN;
+  constexpr uint32_t kCols = Acc<BN>::kCols;
+  constexpr int kSteps = R / 32;  // MMAs (K = 32) per tap and chunk
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -92,19 +124,28 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
   const int halo_stage = p.n_ph * p.HB;
   uint8_t* wreg = halo + p.hs * halo_stage;
   const int wblocks = p.resident ? p.chunks * p.n_taps : p.ws;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(wreg + (size_t)wblocks * p.WB);
+  // epilogue parameter slots (2, by item parity): 6*BN words each
+  // epilogue parameters of all N channels, staged once: int mode
+  // [n_q][3][N] (c0, c1, sign), float mode [2][N] (gain, bias)
+  uint32_t* eparam = reinterpret_cast<uint32_t*>(wreg + (size_t)wblocks * p.WB);
+  const int ewords = p.ithr ? p.n_q * 3 * p.N : 2 * p.N;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(eparam + ((ewords + 1) & ~1));
   uint64_t* h_full = bars;
   uint64_t* h_empty = h_full + p.hs;
   uint64_t* w_full = h_empty + p.hs;
   uint64_t* w_empty = w_full + p.ws;
   uint64_t* a_full = w_empty + p.ws;
-  uint64_t* a_empty = a_full + 2;
-  uint64_t* w_res = a_empty + 2;
+  uint64_t* a_empty = a_full + kAcc;
+  uint64_t* w_res = a_empty + kAcc;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(w_res + 1);
+  // tap A-operand byte offsets and halo phase ids in (static) shared memory:
+  // the issue loops read them with LDS instead of indexing kernel parameters
+  __shared__ uint32_t s_tap[9];
+  __shared__ int s_ph[4];
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  constexpr uint32_t kCols = 2 * BN;  // two accumulators
-  constexpr int kSteps = R / 32;      // MMAs (K = 32) per tap and chunk
+  const bool stamp = (p.dbg & 16) && blockIdx.x < 148;
+  if (stamp && threadIdx.x == 0) g_stamps[blockIdx.x * 8 + 0] = gtime();
 
   if (threadIdx.x == 0) {
     sm100::tma_prefetch(&in_map);
@@ -117,11 +158,15 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
       sm100::mbar_init(&w_full[s], 1);
       sm100::mbar_init(&w_empty[s], 1);
     }
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < kAcc; ++s) {
       sm100::mbar_init(&a_full[s], 1);
-      sm100::mbar_init(&a_empty[s], 128);
+      sm100::mbar_init(&a_empty[s], kEpiThreads / 2);  // one epilogue group per tile
     }
     sm100::mbar_init(w_res, 1);
+#pragma unroll
+    for (int t = 0; t < 9; ++t) s_tap[t] = (uint32_t)(p.tap_slot[t] * p.HB + p.tap_shift[t] * R);
+#pragma unroll
+    for (int s = 0; s < 4; ++s) s_ph[s] = p.ph_id[s];
     sm100::fence_mbar_init();
   }
   if (warp == 1) sm100::tmem_alloc<kCols>(tslot);
@@ -130,131 +175,225 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
   sm100::tc_fence_after();
   const uint32_t tmem = *tslot;
   const int n_items = p.m_tiles * p.n_tiles;
+  // CTAs walk the (chunk, tap) weight blocks from different starting points
+  // (integer sums are order independent) so they do not all hit the same L2
+  // lines at once.
+  const int rot_c = blockIdx.x % p.chunks;
 
-  if (warp == 0 && lane == 0) {
+  // The producer and MMA roles run as WHOLE warps (all lanes wait on the
+  // barriers, lane 0 issues).  Ring positions advance with (stage, round)
+  // counters -- no integer division in the issue loops: a single issuing
+  // thread's dependent scalar latency is what bounds the MMA issue rate.
+  if (warp == 0) {
     // ================= producer =================
-    if (p.resident) {  // all weight blocks of the (single) n-tile, once
+    if (p.resident && lane == 0) {  // all weight blocks of the (single) n-tile, once
       sm100::mbar_arrive_expect_tx(w_res, (uint32_t)(p.chunks * p.n_taps) * BN * R);
       for (int b = 0; b < p.chunks * p.n_taps; ++b)
         sm100::tma_load_2d(wreg + (size_t)b * p.WB, &w_map, w_res, 0, b * BN);
     }
-    int hc = 0, wc = 0;
+    int hs_i = 0, h_round = 0, ws_i = 0, w_round = 0;
+    int mt = blockIdx.x / p.n_tiles, nt = blockIdx.x - mt * p.n_tiles;
+    const int dmt = gridDim.x / p.n_tiles, dnt = gridDim.x - dmt * p.n_tiles;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-      const int mt = item / p.n_tiles, nt = item - mt * p.n_tiles;
       const int row0 = mt * 128 + p.base_shift;
-      for (int ch = 0; ch < p.chunks; ++ch) {
-        const int hsi = hc % p.hs;
-        if (hc >= p.hs) sm100::mbar_wait(&h_empty[hsi], ((hc / p.hs) - 1) & 1);
-        sm100::mbar_arrive_expect_tx(&h_full[hsi], (uint32_t)(p.n_ph * p.halo_rows * R));
-        for (int s = 0; s < p.n_ph; ++s) {
-          const long long r = (long long)(ch * p.in_phases + p.ph_id[s]) * p.in_pos + row0;
-          sm100::tma_load_2d(halo + hsi * halo_stage + s * p.HB, &in_map, &h_full[hsi], 0, (int)r);
-        }
-        ++hc;
-        if (!p.resident) {
-          for (int t = 0; t < p.n_taps; ++t) {
-            const int wsi = wc % p.ws;
-            if (wc >= p.ws) sm100::mbar_wait(&w_empty[wsi], ((wc / p.ws) - 1) & 1);
-            sm100::mbar_arrive_expect_tx(&w_full[wsi], BN * R);
-            const int blk = (nt * p.chunks + ch) * p.n_taps + t;
-            sm100::tma_load_2d(wreg + (size_t)wsi * p.WB, &w_map, &w_full[wsi], 0, blk * BN);
-            ++wc;
+      int ch = rot_c;
+      for (int ci = 0; ci < p.chunks; ++ci) {
+        if (h_round) sm100::mbar_wait(&h_empty[hs_i], (h_round - 1) & 1);
+        if (lane == 0) {
+          if (stamp && blockIdx.x == 0 && h_round * p.hs + hs_i < 32)
+            g_trace[0 * 32 + h_round * p.hs + hs_i] = clock64();
+          if (p.dbg & 2) {
+            sm100::mbar_arrive(&h_full[hs_i]);
+          } else {
+            sm100::mbar_arrive_expect_tx(&h_full[hs_i], (uint32_t)(p.n_ph * p.halo_rows * R));
+            const long long rbase = (long long)ch * p.in_phases * p.in_pos + row0;
+            for (int s2 = 0; s2 < p.n_ph; ++s2)
+              sm100::tma_load_2d(halo + hs_i * halo_stage + s2 * p.HB, &in_map, &h_full[hs_i], 0,
+                                 (int)(rbase + (long long)s_ph[s2] * p.in_pos));
           }
         }
+        __syncwarp();
+        if (++hs_i == p.hs) { hs_i = 0; ++h_round; }
+        if (!p.resident) {
+          const int blk0 = (nt * p.chunks + ch) * KT;
+          for (int t = 0; t < KT; ++t) {
+            if (w_round) sm100::mbar_wait(&w_empty[ws_i], (w_round - 1) & 1);
+            if (lane == 0) {
+              sm100::mbar_arrive_expect_tx(&w_full[ws_i], BN * R);
+              sm100::tma_load_2d(wreg + (size_t)ws_i * p.WB, &w_map, &w_full[ws_i], 0, (blk0 + t) * BN);
+            }
+            __syncwarp();
+            if (++ws_i == p.ws) { ws_i = 0; ++w_round; }
+          }
+        }
+        if (++ch == p.chunks) ch = 0;
       }
+      mt += dmt;
+      nt += dnt;
+      if (nt >= p.n_tiles) { nt -= p.n_tiles; ++mt; }
     }
-  } else if (warp == 1 && lane == 0) {
-    // ================= MMA issuer =================
+  } else if (warp == 1) {
+    // ================= MMA issuer (warp-uniform, elect.sync issues) ======
     constexpr uint32_t idesc = sm100::idesc_i8(128, BN);
+    if (stamp && lane == 0) g_stamps[blockIdx.x * 8 + 1] = gtime();
     if (p.resident) sm100::mbar_wait(w_res, 0);
-    int hc = 0, wc = 0, it = 0;
+    if (stamp && lane == 0) g_stamps[blockIdx.x * 8 + 2] = gtime();
+    // descriptor templates: only the start-address field (bits 0-13, in
+    // 16-byte units) changes per MMA
+    const uint64_t tmpl = desc_sw(0, R);
+    const uint32_t halo0 = sm100::smem_u32(halo), wreg0 = sm100::smem_u32(wreg);
+    uint32_t toff[KT];
+#pragma unroll
+    for (int t = 0; t < KT; ++t) toff[t] = (uint32_t)(p.tap_slot[t] * p.HB + p.tap_shift[t] * R);
+    const bool do_mma = !(p.dbg & 1);
+    int hs_i = 0, h_round = 0, ws_i = 0, w_round = 0, acc = 0, a_round = 0, it = 0;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
-      const int acc = it & 1;
-      if (it >= 2) sm100::mbar_wait(&a_empty[acc], ((it >> 1) - 1) & 1);
+      if (a_round) sm100::mbar_wait(&a_empty[acc], (a_round - 1) & 1);
+      if (stamp && lane == 0 && blockIdx.x == 0 && it < 32) g_trace[1 * 32 + it] = clock64();
       sm100::tc_fence_after();
       const uint32_t d = tmem + acc * BN;
-      for (int ch = 0; ch < p.chunks; ++ch) {
-        const int hsi = hc % p.hs;
-        sm100::mbar_wait(&h_full[hsi], (hc / p.hs) & 1);
+      int ch = rot_c;
+      for (int ci = 0; ci < p.chunks; ++ci) {
+        sm100::mbar_wait(&h_full[hs_i], h_round & 1);
+        if (stamp && lane == 0 && blockIdx.x == 0 && h_round * p.hs + hs_i < 32)
+          g_trace[2 * 32 + h_round * p.hs + hs_i] = clock64();
         sm100::tc_fence_after();
-        const uint32_t hbase = sm100::smem_u32(halo + hsi * halo_stage);
-        for (int t = 0; t < p.n_taps; ++t) {
-          uint32_t wb;
-          int wsi = 0;
-          if (p.resident) {
-            wb = sm100::smem_u32(wreg + (size_t)(ch * p.n_taps + t) * p.WB);
-          } else {
-            wsi = wc % p.ws;
-            sm100::mbar_wait(&w_full[wsi], (wc / p.ws) & 1);
-            sm100::tc_fence_after();
-            wb = sm100::smem_u32(wreg + (size_t)wsi * p.WB);
-          }
-          const uint32_t ab = hbase + p.tap_slot[t] * p.HB + p.tap_shift[t] * R;
+        const uint32_t hbase = halo0 + hs_i * halo_stage;
+        const uint32_t wres = wreg0 + (uint32_t)(ch * KT) * p.WB;
 #pragma unroll
-          for (int k = 0; k < kSteps; ++k)
-            sm100::mma_i8(d, desc_sw(ab + k * 32, R), desc_sw(wb + k * 32, R), idesc,
-                          (ch | t | k) != 0);
+        for (int t = 0; t < KT; ++t) {
+          uint32_t wb;
+          if (p.resident) {
+            wb = wres + (uint32_t)t * p.WB;
+          } else {
+            sm100::mbar_wait(&w_full[ws_i], w_round & 1);
+            sm100::tc_fence_after();
+            wb = wreg0 + (uint32_t)ws_i * p.WB;
+          }
+          const uint32_t ab = hbase + toff[t];
+          if (do_mma) {
+#pragma unroll
+            for (int k = 0; k < kSteps; ++k)
+              sm100::mma_i8_elect(d, tmpl | (uint64_t)(((ab + k * 32) & 0x3FFFFu) >> 4),
+                                  tmpl | (uint64_t)(((wb + k * 32) & 0x3FFFFu) >> 4), idesc,
+                                  (ci | t | k) != 0);
+          }
           if (!p.resident) {
-            sm100::mma_commit(&w_empty[wsi]);
-            ++wc;
+            sm100::mma_commit_elect(&w_empty[ws_i]);
+            if (++ws_i == p.ws) { ws_i = 0; ++w_round; }
           }
         }
-        sm100::mma_commit(&h_empty[hsi]);
-        ++hc;
+        if (stamp && lane == 0 && blockIdx.x == 0 && h_round * p.hs + hs_i < 32)
+          g_trace[4 * 32 + h_round * p.hs + hs_i] = clock64();
+        sm100::mma_commit_elect(&h_empty[hs_i]);
+        if (++hs_i == p.hs) { hs_i = 0; ++h_round; }
+        if (++ch == p.chunks) ch = 0;
       }
-      sm100::mma_commit(&a_full[acc]);
+      sm100::mma_commit_elect(&a_full[acc]);
+      if (++acc == kAcc) { acc = 0; ++a_round; }
     }
+    if (stamp && lane == 0) g_stamps[blockIdx.x * 8 + 3] = gtime();
   } else if (warp >= 2) {
-    // ================= epilogue =================
+    // ================= epilogue =========================================
+    // two groups of 4 warps take alternate tiles (two tiles in flight hide
+    // the TMEM-load and store latencies); within a group warp w owns TMEM
+    // lane quarter w % 4 and walks all BN columns.
+    const int et = threadIdx.x - 64;  // 0..255
     const int qtr = warp & 3;
+    const int grp = (warp - 2) >> 2;
     const int plane = p.PHg * p.PWg;
+    const long long oplane = (long long)p.Ho * p.Wo;
+    for (int i = et; i < ewords; i += kEpiThreads)
+      eparam[i] = p.ithr ? (uint32_t)__ldg(p.ithr + i)
+                         : __float_as_uint(__ldg((i < p.N ? p.gain : p.bias - p.N) + i));
+    epi_bar();
+    const uint32_t* ep = eparam;
     int it = 0;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
+      if ((it & 1) != grp) continue;
       const int mt = item / p.n_tiles, nt = item - mt * p.n_tiles;
-      const int acc = it & 1;
-      const long long qrow = (long long)mt * 128 + qtr * 32 + lane;
-      const int img = (int)(qrow / plane);
-      const int rem = (int)(qrow - (long long)img * plane);
+      const int acc = it % kAcc;
+      if (p.dbg & 8) {  // profiling: bare accumulator hand-off
+        if (!(p.dbg & 64) || lane == 0) sm100::mbar_wait(&a_full[acc], (it / kAcc) & 1);
+        __syncwarp();
+        if (stamp && blockIdx.x == 0 && it < 32 && qtr == 0 && lane == 0) g_trace[3 * 32 + it] = clock64();
+        sm100::tc_fence_after();
+        sm100::tc_fence_before();
+        sm100::mbar_arrive(&a_empty[acc]);
+        continue;
+      }
+      const int qrow = mt * 128 + qtr * 32 + lane;  // m_total < 2^31 (checked at setup)
+      const int img = qrow / plane;
+      const int rem = qrow - img * plane;
       const int oy = rem / p.PWg, ox = rem - (rem / p.PWg) * p.PWg;
       const bool valid = qrow < p.m_total && oy < p.Ho && ox < p.Wo;
       const long long P1 = ((long long)img * p.o_Hp + oy + 1) * p.o_Wp + ox + 1;
       const int py = oy + 1, px = ox + 1;
       const long long P4 = ((long long)img * p.o_PH + (py >> 1)) * p.o_PW + (px >> 1);
       const int ph4 = (py & 1) * 2 + (px & 1);
-      sm100::mbar_wait(&a_full[acc], (it >> 1) & 1);
+      // NCHW index of (img, channel 0, oy, ox) in the f32 skip / output tensors
+      const long long fbase = (long long)img * p.N * oplane + (long long)oy * p.Wo + ox;
+      sm100::mbar_wait(&a_full[acc], (it / kAcc) & 1);
       sm100::tc_fence_after();
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 32) {
         uint32_t r[32];
         sm100::tmem_ld32(tmem + ((uint32_t)(qtr * 32) << 16) + acc * BN + c0, r);
         sm100::tmem_ld_wait();
-        if (!valid) continue;
+        if (!valid || (p.dbg & 4)) continue;
         const int n0 = nt * BN + c0;
+        if (p.ithr) {
+          // integer-threshold epilogue: level = (s*acc > c0) + (s*acc > c1)
+#pragma unroll
+          for (int o = 0; o < 2; ++o) {
+            if (o >= p.n_q) break;
+            const int* e0 = reinterpret_cast<const int*>(ep) + o * 3 * p.N + n0;
+            uint32_t w[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              uint32_t b = 0;
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const int c = 4 * j + i;
+                const int x = (int)r[c] * e0[2 * p.N + c];
+                b |= ((uint32_t)(x > e0[c]) + (uint32_t)(x > e0[p.N + c])) << (8 * i);
+              }
+              w[j] = b;
+            }
+            const int Rq = p.q_R[o];
+            const int chq = n0 / Rq, cq = n0 - chq * Rq;
+            const long long off = p.q_phases[o] == 4 ? ((long long)(chq * 4 + ph4) * p.q_pos[o] + P4) * Rq + cq
+                                                     : ((long long)chq * p.q_pos[o] + P1) * Rq + cq;
+            uint4* dst = reinterpret_cast<uint4*>(p.q[o] + off);
+            dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
+            dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+          }
+          continue;
+        }
+        const float* eg = reinterpret_cast<const float*>(ep) + n0;
         float v[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
           // R:linalg.hpp:322-323 (FMA-contracted like the reference build)
-          v[j] = __fmaf_rn(__ldg(p.gain + n0 + j), __fmul_rn(p.out_scale, (float)(int32_t)r[j]),
-                           __ldg(p.bias + n0 + j));
+          v[j] = __fmaf_rn(eg[j], __fmul_rn(p.out_scale, (float)(int32_t)r[j]), eg[p.N + j]);
         }
-        if (p.skip) {
-          const float4* s4 = reinterpret_cast<const float4*>(p.skip + ((long long)(n0 >> 5) * p.f_pos + P1) * 32);
+        if (p.skip) {  // NCHW: lanes = consecutive positions -> coalesced per channel
+          const float* s = p.skip + fbase + (long long)n0 * oplane;
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const float4 s = __ldg(s4 + j);
-            v[4 * j] += s.x; v[4 * j + 1] += s.y; v[4 * j + 2] += s.z; v[4 * j + 3] += s.w;
-          }
+          for (int j = 0; j < 32; ++j) v[j] += __ldg(s + j * oplane);
         }
         if (p.relu) {
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = v[j] < 0.0f ? 0.0f : v[j];  // std::max(v, 0.0f)
         }
         if (p.fout) {
-          float4* o4 = reinterpret_cast<float4*>(p.fout + ((long long)(n0 >> 5) * p.f_pos + P1) * 32);
+          float* o = p.fout + fbase + (long long)n0 * oplane;
 #pragma unroll
-          for (int j = 0; j < 8; ++j) o4[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          for (int j = 0; j < 32; ++j) o[j * oplane] = v[j];
         }
-        for (int o = 0; o < p.n_q; ++o) {
+#pragma unroll
+        for (int o = 0; o < 2; ++o) {
+          if (o >= p.n_q) break;
           uint32_t w[8];
           bool bad = false;
 #pragma unroll
@@ -272,11 +411,8 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
           if (bad) tk_raise(p.err, (unsigned long long)qrow, TK_ERR_NONFINITE);
           const int Rq = p.q_R[o];
           const int chq = n0 / Rq, cq = n0 - chq * Rq;
-          long long off;
-          if (p.q_phases[o] == 4)
-            off = ((long long)(chq * 4 + ph4) * p.q_pos[o] + P4) * Rq + cq;
-          else
-            off = ((long long)chq * p.q_pos[o] + P1) * Rq + cq;
+          const long long off = p.q_phases[o] == 4 ? ((long long)(chq * 4 + ph4) * p.q_pos[o] + P4) * Rq + cq
+                                                   : ((long long)chq * p.q_pos[o] + P1) * Rq + cq;
           uint4* dst = reinterpret_cast<uint4*>(p.q[o] + off);
           dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
           dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
@@ -285,57 +421,53 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
       sm100::tc_fence_before();
       sm100::mbar_arrive(&a_empty[acc]);
     }
+    if (stamp && warp == 2 && lane == 0) g_stamps[blockIdx.x * 8 + 4] = gtime();
   }
   sm100::tc_fence_before();
   __syncthreads();
   if (warp == 1) sm100::tmem_dealloc<kCols>(tmem);
+  if (stamp && threadIdx.x == 0) g_stamps[blockIdx.x * 8 + 5] = gtime();
 }
 
 // ---------------------------------------------------------------------------
-// input packing: NCHW f32 -> s8 level tensors (up to 2 variants) + f32 copy.
+// input packing: NCHW f32 -> s8 level tensors (up to 2 variants).  One thread
+// per (image, 16-channel group, position): 16 loads coalesced across the warp
+// (consecutive positions), one 16-byte store per variant.
 struct PackIn {
   const float* x;
-  int C, H, W;
+  int N, C, H, W;
   int n_q;
   int8_t* q[2];
   float t0[2], t1[2];
   int q_phases[2], q_R[2];
   long long q_pos[2];
   int Hp, Wp, PH, PW;
-  float* f;
-  long long f_pos;
   unsigned long long* err;
 };
 
-// one block per (image, row): stage the row's C x W floats in SMEM, then
-// write channel-contiguous level bytes / float groups per position.
 __global__ void k_pack_input(const PackIn p) {
-  extern __shared__ float srow[];  // [C][W + 1]
-  const int n = blockIdx.x / p.H, y = blockIdx.x - (blockIdx.x / p.H) * p.H;
-  const int Wp1 = p.W + 1;
-  for (int i = threadIdx.x; i < p.C * p.W; i += blockDim.x) {
-    const int c = i / p.W, xx = i - c * p.W;
-    srow[c * Wp1 + xx] = __ldg(p.x + (((long long)n * p.C + c) * p.H + y) * p.W + xx);
-  }
-  __syncthreads();
-  // 16-channel groups per position
+  const long long HW = (long long)p.H * p.W;
   const int groups = p.C / 16;
-  for (int i = threadIdx.x; i < groups * p.W; i += blockDim.x) {
-    const int g = i / p.W, xx = i - g * p.W;  // xx fastest -> coalesced-ish rows
+  const long long total = (long long)p.N * groups * HW;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long pix = i % HW;
+    const long long t = i / HW;
+    const int g = (int)(t % groups), n = (int)(t / groups);
+    const int y = (int)(pix / p.W), xx = (int)(pix - (long long)y * p.W);
+    const float* src = p.x + ((long long)n * p.C + g * 16) * HW + pix;
     float v[16];
     bool bad = false;
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
-      v[j] = srow[(g * 16 + j) * Wp1 + xx];
+      v[j] = __ldg(src + j * HW);
       bad |= !(v[j] >= 0.0f && v[j] <= 3.402823466e38f);
     }
     if (bad) {
+#pragma unroll
       for (int j = 0; j < 16; ++j) {
         const int e = tk_error_code(v[j], 1);
-        if (e != TK_OK) {
-          tk_raise(p.err, (((unsigned long long)n * p.C + g * 16 + j) * p.H + y) * p.W + xx, e);
-          break;
-        }
+        if (e != TK_OK) tk_raise(p.err, (unsigned long long)(((long long)n * p.C + g * 16 + j) * HW + pix), e);
       }
     }
     const int py = y + 1, px = xx + 1;
@@ -360,42 +492,7 @@ __global__ void k_pack_input(const PackIn p) {
                                                : ((long long)chq * p.q_pos[o] + P1) * Rq + cq;
       *reinterpret_cast<uint4*>(p.q[o] + off) = make_uint4(w[0], w[1], w[2], w[3]);
     }
-    if (p.f) {
-      float4* o4 = reinterpret_cast<float4*>(p.f + ((long long)(g >> 1) * p.f_pos + P1) * 32 + (g & 1) * 16);
-#pragma unroll
-      for (int j = 0; j < 4; ++j) o4[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-    }
   }
-}
-
-// f32 [C/32][pos][32] -> NCHW
-__global__ void k_unpack_f32(const float* __restrict__ f, long long f_pos, int N, int C, int H, int W,
-                             int Hp, int Wp, float* __restrict__ out) {
-  const long long total = (long long)N * C * H * W;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
-    const int xx = (int)(i % W);
-    long long t = i / W;
-    const int y = (int)(t % H);
-    t /= H;
-    const int c = (int)(t % C);
-    const int n = (int)(t / C);
-    const long long P1 = ((long long)n * Hp + y + 1) * Wp + xx + 1;
-    out[i] = f[((long long)(c >> 5) * f_pos + P1) * 32 + (c & 31)];
-  }
-}
-
-// spatial mean of the f32 layout -> [N][C] (head input; left-to-right sum)
-__global__ void k_pool_f32(const float* __restrict__ f, long long f_pos, int N, int C, int H, int W, int Hp,
-                           int Wp, float* __restrict__ out) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= N * C) return;
-  const int n = i / C, c = i - (i / C) * C;
-  float s = 0.0f;
-  for (int y = 0; y < H; ++y)
-    for (int xx = 0; xx < W; ++xx)
-      s += f[((long long)(c >> 5) * f_pos + ((long long)n * Hp + y + 1) * Wp + xx + 1) * 32 + (c & 31)];
-  out[i] = s / (float)(H * W);
 }
 
 // generic path helpers (NCHW)
@@ -406,6 +503,7 @@ __global__ void k_residual_relu(float* __restrict__ z, const float* __restrict__
   }
 }
 
+// spatial mean -> [N][C] (head input; left-to-right float sum)
 __global__ void k_pool_nchw(const float* __restrict__ x, int NC, int HW, float* __restrict__ out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= NC) return;
@@ -454,10 +552,10 @@ struct S8T {  // s8 level tensor
   float ta1 = 0, ta2 = 0;
   size_t bytes() const { return (size_t)(C / R) * phases * pos * R; }
 };
-struct F32T {
+struct F32T {  // f32 NCHW tensor
   float* p = nullptr;
-  int C = 0, H = 0, W = 0, Hp = 0, Wp = 0;
-  long long pos = 0;
+  int C = 0, H = 0, W = 0;
+  long long elems = 0;
 };
 
 int pick_R(int C) { return C == 64 ? 64 : 128; }
@@ -478,10 +576,11 @@ struct Conv {
   int8_t* d_w = nullptr;  // [nt][ch][tap][BN][R]
   float* d_gain = nullptr;
   float* d_bias = nullptr;
+  int* d_ithr = nullptr;
   tk_layer* layer = nullptr;  // generic path
   // fused wiring
   int in_idx = -1;            // index into net->s8
-  int skip_f = -1, out_f = -1;
+  int skip_f = -1, out_f = -1;  // -2 = the forward's input tensor
   int q_idx[2] = {-1, -1};
   int relu = 0;
   ConvK k{};
@@ -498,15 +597,13 @@ struct tk_net {
   int batch = 0, in_c = 0, in_h = 0, in_w = 0;
   int out_c = 0, out_h = 0, out_w = 0;
   std::vector<tk_block_desc> blocks;
-  std::vector<std::vector<Conv>> convs;  // per block: convs..., then down
+  std::vector<std::vector<Conv>> convs;  // fused: down first; generic: convs then down
   std::vector<S8T> s8;
   std::vector<F32T> f32;
   PackIn pack{};
   int final_f = -1;
-  // generic path buffers
-  std::vector<float*> gbuf;
+  std::vector<float*> gbuf;  // generic path buffers
   size_t gbuf_elems = 0;
-  float* d_pool_tmp = nullptr;
 };
 
 namespace {
@@ -567,7 +664,7 @@ void plan_taps(Conv& cv, const S8T& in) {
   int used[4] = {0, 0, 0, 0};
   for (int i = 0; i < n; ++i) used[phs[i]] = 1;
   k.n_ph = 0;
-  int slot_of[4];
+  int slot_of[4] = {0, 0, 0, 0};
   for (int ph = 0; ph < 4; ++ph)
     if (used[ph]) { slot_of[ph] = k.n_ph; k.ph_id[k.n_ph++] = ph; }
   int mn = 1 << 30, mx = 0;
@@ -623,33 +720,57 @@ int prepare_conv_weights(Conv& cv, int R) {
   return TK_OK;
 }
 
-// s8 tensor index for (C, H, W, phases, ta) -- reuse or create
-int want_s8(tk_net* net, int C, int H, int W, int phases, float ta1, float ta2) {
-  for (size_t i = 0; i < net->s8.size(); ++i) {
-    const S8T& t = net->s8[i];
-    (void)t;
+// The exact float epilogue of an inner conv, as the kernel (and the
+// reference build) computes it: max(fma(g, s*acc, b), 0).
+float epi_value(float g, float s, float b, int acc) {
+  volatile float prod = s * (float)acc;  // rounded product, no contraction
+  return fmaf(g, prod, b);
+}
+
+// Integer thresholds reproducing (relu(v(acc)) > t) for t >= 0 exactly:
+// bit = (sign*acc > c).  v is monotone in acc (direction = sign of g*s).
+void int_threshold(float g, float s, float b, float t, int kmax, int* c, int* sign) {
+  const bool up = (g >= 0.0f) == (s >= 0.0f);
+  auto pred = [&](int a) { return epi_value(g, s, b, a) > t; };
+  if (up) {  // pred false..true: c = largest acc with !pred
+    int lo = -kmax - 1, hi = kmax + 1;  // treat lo as !pred, hi as pred
+    while (hi - lo > 1) {
+      const int mid = lo + (hi - lo) / 2;
+      if (pred(mid)) hi = mid; else lo = mid;
+    }
+    *c = lo;
+    *sign = 1;
+  } else {  // pred true..false: bit = acc < B, B = smallest acc with !pred
+    int lo = -kmax - 1, hi = kmax + 1;  // lo as pred, hi as !pred
+    while (hi - lo > 1) {
+      const int mid = lo + (hi - lo) / 2;
+      if (pred(mid)) lo = mid; else hi = mid;
+    }
+    *c = -hi;
+    *sign = -1;
   }
+}
+
+int want_s8(tk_net* net, int C, int H, int W, int phases, float ta1, float ta2) {
   net->s8.push_back(make_s8(net->batch, C, H, W, phases, ta1, ta2));
   return (int)net->s8.size() - 1;
 }
 
 int want_f32(tk_net* net, int C, int H, int W) {
   F32T f;
-  f.C = C; f.H = H; f.W = W; f.Hp = H + 2; f.Wp = W + 2;
-  f.pos = (long long)net->batch * f.Hp * f.Wp;
+  f.C = C; f.H = H; f.W = W;
+  f.elems = (long long)net->batch * C * H * W;
   net->f32.push_back(f);
   return (int)net->f32.size() - 1;
 }
 
 int setup_fused(tk_net* net) {
-  // ---- wiring: consumers of each block input / intermediate ----
   int H = net->in_h, W = net->in_w, C = net->in_c;
   const int nb = (int)net->blocks.size();
-  // block-input tensors: variants needed by conv1 and down
   struct In { int idx_conv1, idx_down, f; };
   std::vector<In> bin(nb);
   auto phases_of = [](const tk_conv_desc& d) { return d.stride == 2 ? 4 : 1; };
-  // block inputs
+  // block inputs: s8 variants for conv1 / down, f32 for identity shortcuts
   for (int b = 0; b < nb; ++b) {
     const tk_block_desc& bd = net->blocks[b];
     const tk_conv_desc& c1 = bd.conv[0];
@@ -662,14 +783,14 @@ int setup_fused(tk_net* net) {
       else
         bin[b].idx_down = want_s8(net, C, H, W, phases_of(dn), dn.ta1, dn.ta2);
     }
-    bin[b].f = bd.has_down ? -1 : want_f32(net, C, H, W);
+    bin[b].f = bd.has_down ? -1 : (b == 0 ? -2 : want_f32(net, C, H, W));
     int h = H, w = W;
     for (int i = 0; i < bd.n_convs; ++i) { h = conv_out(h, bd.conv[i]); w = conv_out(w, bd.conv[i]); }
     H = h; W = w; C = bd.conv[bd.n_convs - 1].out_c;
   }
   net->out_c = C; net->out_h = H; net->out_w = W;
   net->final_f = want_f32(net, C, H, W);
-  // ---- convs ----
+  // convs (the downsample first: its f32 output is the block's residual)
   H = net->in_h; W = net->in_w; C = net->in_c;
   net->convs.assign(nb, {});
   for (int b = 0; b < nb; ++b) {
@@ -678,7 +799,7 @@ int setup_fused(tk_net* net) {
     int cur = bin[b].idx_conv1;
     int h = H, w = W, c = C;
     int sc_f = bin[b].f;
-    if (bd.has_down) {  // shortcut first: its f32 output is the residual
+    if (bd.has_down) {
       Conv dv;
       dv.d = bd.down;
       dv.in_idx = bin[b].idx_down;
@@ -692,19 +813,18 @@ int setup_fused(tk_net* net) {
       cv.d = d;
       cv.in_idx = cur;
       const int ho = conv_out(h, d), wo = conv_out(w, d);
+      cv.relu = 1;
       if (i + 1 < bd.n_convs) {
-        cv.relu = 1;
         const tk_conv_desc& nx = bd.conv[i + 1];
         cv.q_idx[0] = want_s8(net, d.out_c, ho, wo, phases_of(nx), nx.ta1, nx.ta2);
         cur = cv.q_idx[0];
       } else {
-        cv.relu = 1;
         cv.skip_f = sc_f;
         if (b + 1 < nb) {
           cv.q_idx[0] = bin[b + 1].idx_conv1;
           if (bin[b + 1].idx_down >= 0 && bin[b + 1].idx_down != bin[b + 1].idx_conv1)
             cv.q_idx[1] = bin[b + 1].idx_down;
-          cv.out_f = bin[b + 1].f;  // identity shortcut of the next block
+          cv.out_f = bin[b + 1].f;  // identity shortcut of the next block (or -1)
         } else {
           cv.out_f = net->final_f;
         }
@@ -714,14 +834,14 @@ int setup_fused(tk_net* net) {
     }
     H = h; W = w; C = c;
   }
-  // ---- allocate tensors ----
+  // allocate tensors
   for (auto& t : net->s8) {
     if (cudaMalloc(&t.p, t.bytes()) != cudaSuccess) return TK_ERR_CUDA;
     cudaMemset(t.p, 0, t.bytes());  // pad ring = code of quantize(0.0) = level 0
   }
   for (auto& f : net->f32)
-    if (cudaMalloc(&f.p, (size_t)f.C * f.pos * 4) != cudaSuccess) return TK_ERR_CUDA;
-  // ---- per-conv kernel parameters ----
+    if (cudaMalloc(&f.p, (size_t)f.elems * 4) != cudaSuccess) return TK_ERR_CUDA;
+  // per-conv kernel parameters
   for (auto& cvs : net->convs)
     for (auto& cv : cvs) {
       const S8T& in = net->s8[cv.in_idx];
@@ -732,27 +852,28 @@ int setup_fused(tk_net* net) {
       k.n_tiles = cv.n_tiles;
       k.m_total = (long long)net->batch * k.PHg * k.PWg;
       k.m_tiles = (int)((k.m_total + 127) / 128);
+      if (k.m_total + 1024 > (1ll << 31)) return TK_ERR_UNSUPPORTED;  // 32-bit row indices
       k.HB = (k.halo_rows * cv.R + 1023) / 1024 * 1024;
       k.WB = (cv.BN * cv.R + 1023) / 1024 * 1024;
-      const int budget = 200 * 1024;
+      const int budget = 224 * 1024 - 6 * cv.d.out_c * 4 - 1536;  // of 227 KB dynamic SMEM
       const int halo_stage = k.n_ph * k.HB;
-      k.hs = 2 * halo_stage + 4 * k.WB <= budget ? 2 : 1;
       const int wbytes_all = cv.chunks * k.n_taps * k.WB;
-      k.resident = (cv.n_tiles == 1 && k.hs * halo_stage + wbytes_all <= budget) ? 1 : 0;
+      k.resident = (cv.n_tiles == 1 && 2 * halo_stage + wbytes_all <= budget) ? 1 : 0;
+      const int wmin = k.resident ? wbytes_all : 3 * k.WB;
+      k.hs = std::max(1, std::min(4, (budget - wmin) / halo_stage));
       k.ws = k.resident ? 1 : std::max(2, std::min(8, (budget - k.hs * halo_stage) / k.WB));
       const int wregion = k.resident ? wbytes_all : k.ws * k.WB;
-      cv.smem = 1024 + k.hs * halo_stage + wregion + 512;
+      // epilogue parameter words: at most 2 quantized outputs x 3 ints per channel
+      cv.smem = 1024 + k.hs * halo_stage + wregion + 6 * cv.d.out_c * 4 + 512;
       k.gain = cv.d_gain;
       k.bias = cv.d_bias;
       k.out_scale = cv.d.out_scale;
       k.relu = cv.relu;
       k.N = cv.d.out_c;
-      const int ho = k.Ho, wo = k.Wo;
-      k.o_Hp = ho + 2; k.o_Wp = wo + 2;
+      k.o_Hp = k.Ho + 2; k.o_Wp = k.Wo + 2;
       k.o_PH = k.o_Hp / 2; k.o_PW = k.o_Wp / 2;
-      k.skip = cv.skip_f >= 0 ? net->f32[cv.skip_f].p : nullptr;
+      k.skip = cv.skip_f >= 0 ? net->f32[cv.skip_f].p : nullptr;  // -2: patched at launch
       k.fout = cv.out_f >= 0 ? net->f32[cv.out_f].p : nullptr;
-      k.f_pos = (long long)net->batch * k.o_Hp * k.o_Wp;
       k.n_q = 0;
       for (int o = 0; o < 2; ++o) {
         if (cv.q_idx[o] < 0) continue;
@@ -767,15 +888,38 @@ int setup_fused(tk_net* net) {
         k.q_pos[k.n_q] = q.pos;
         ++k.n_q;
       }
+      // integer-threshold epilogue for inner convs (ReLU + quantize only)
+      k.ithr = nullptr;
+      if (cv.relu && cv.skip_f == -1 && cv.out_f < 0 && k.n_q > 0 && k.t0[0] >= 0.0f) {
+        const int N = cv.d.out_c, kmax = 2 * cv.d.in_c * cv.d.k * cv.d.k;
+        std::vector<int> thr((size_t)k.n_q * 3 * N);
+        std::vector<float> g(N, 1.0f), b(N, 0.0f);
+        if (cv.d.gain_host) memcpy(g.data(), cv.d.gain_host, N * 4);
+        if (cv.d.bias_host) memcpy(b.data(), cv.d.bias_host, N * 4);
+        for (int o = 0; o < k.n_q; ++o)
+          for (int n = 0; n < N; ++n) {
+            int c0, s0, c1, s1;
+            int_threshold(g[n], cv.d.out_scale, b[n], k.t0[o], kmax, &c0, &s0);
+            int_threshold(g[n], cv.d.out_scale, b[n], k.t1[o], kmax, &c1, &s1);
+            thr[((size_t)o * 3 + 0) * N + n] = c0;
+            thr[((size_t)o * 3 + 1) * N + n] = c1;
+            thr[((size_t)o * 3 + 2) * N + n] = s0;  // s0 == s1 (same direction)
+          }
+        if (cudaMalloc(&cv.d_ithr, thr.size() * 4) != cudaSuccess) return TK_ERR_CUDA;
+        cudaMemcpy(cv.d_ithr, thr.data(), thr.size() * 4, cudaMemcpyHostToDevice);
+        k.ithr = cv.d_ithr;
+      }
       k.err = net->ctx->d_err;
+      k.dbg = getenv("TK_CONV_DBG") ? atoi(getenv("TK_CONV_DBG")) : 0;
       if (!map_rows(&cv.in_map, in.p, (unsigned long long)(in.C / in.R) * in.phases * in.pos, in.R, k.halo_rows))
         return TK_ERR_CUDA;
       const int items = k.m_tiles * k.n_tiles;
       cv.grid = std::min(items, net->ctx->num_sms);
+      if (getenv("TK_CONV_GRID")) cv.grid = std::min(items, atoi(getenv("TK_CONV_GRID")));  // profiling
     }
-  // ---- input packing ----
+  // input packing
   PackIn& pk = net->pack;
-  pk.C = net->in_c; pk.H = net->in_h; pk.W = net->in_w;
+  pk.N = net->batch; pk.C = net->in_c; pk.H = net->in_h; pk.W = net->in_w;
   const S8T& s0 = net->s8[bin[0].idx_conv1];
   pk.Hp = s0.Hp; pk.Wp = s0.Wp; pk.PH = s0.Hp / 2; pk.PW = s0.Wp / 2;
   pk.n_q = 0;
@@ -789,32 +933,38 @@ int setup_fused(tk_net* net) {
     pk.q_phases[pk.n_q] = q.phases; pk.q_R[pk.n_q] = q.R; pk.q_pos[pk.n_q] = q.pos;
     ++pk.n_q;
   }
-  pk.f = bin[0].f >= 0 ? net->f32[bin[0].f].p : nullptr;
-  pk.f_pos = bin[0].f >= 0 ? net->f32[bin[0].f].pos : 0;
   pk.err = net->ctx->d_err;
   return TK_OK;
 }
 
-template <int BN, int R>
-cudaError_t launch_conv(const Conv& cv, cudaStream_t s) {
+template <int BN, int R, int KT>
+cudaError_t launch_conv(const Conv& cv, const float* x, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_conv_tc<BN, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    // 227 KB per block, less the kernel's static shared tables
+    cudaFuncSetAttribute(k_conv_tc<BN, R, KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024);
     attr = true;
   }
-  k_conv_tc<BN, R><<<cv.grid, kConvThreads, cv.smem, s>>>(cv.in_map, cv.w_map, cv.k);
+  ConvK k = cv.k;
+  if (cv.skip_f == -2) k.skip = x;  // identity shortcut = the forward's input
+  k_conv_tc<BN, R, KT><<<cv.grid, kConvThreads, cv.smem, s>>>(cv.in_map, cv.w_map, k);
   return cudaGetLastError();
 }
 
-cudaError_t run_conv(const Conv& cv, cudaStream_t s) {
+template <int KT>
+cudaError_t run_conv_kt(const Conv& cv, const float* x, cudaStream_t s) {
   if (cv.R == 64) {
-    if (cv.BN == 64) return launch_conv<64, 64>(cv, s);
-    if (cv.BN == 128) return launch_conv<128, 64>(cv, s);
-    return launch_conv<256, 64>(cv, s);
+    if (cv.BN == 64) return launch_conv<64, 64, KT>(cv, x, s);
+    if (cv.BN == 128) return launch_conv<128, 64, KT>(cv, x, s);
+    return launch_conv<256, 64, KT>(cv, x, s);
   }
-  if (cv.BN == 64) return launch_conv<64, 128>(cv, s);
-  if (cv.BN == 128) return launch_conv<128, 128>(cv, s);
-  return launch_conv<256, 128>(cv, s);
+  if (cv.BN == 64) return launch_conv<64, 128, KT>(cv, x, s);
+  if (cv.BN == 128) return launch_conv<128, 128, KT>(cv, x, s);
+  return launch_conv<256, 128, KT>(cv, x, s);
+}
+
+cudaError_t run_conv(const Conv& cv, const float* x, cudaStream_t s) {
+  return cv.k.n_taps == 9 ? run_conv_kt<9>(cv, x, s) : run_conv_kt<1>(cv, x, s);
 }
 
 int setup_generic(tk_net* net) {
@@ -904,7 +1054,7 @@ int tk_net_destroy(tk_net* net) {
   cudaDeviceSynchronize();
   for (auto& cvs : net->convs)
     for (auto& cv : cvs) {
-      cudaFree(cv.d_w); cudaFree(cv.d_gain); cudaFree(cv.d_bias);
+      cudaFree(cv.d_w); cudaFree(cv.d_gain); cudaFree(cv.d_bias); cudaFree(cv.d_ithr);
       if (cv.layer) tk_layer_destroy(cv.layer);
     }
   for (auto& t : net->s8) cudaFree(t.p);
@@ -924,6 +1074,16 @@ int tk_net_out_shape(const tk_net* net, int* c, int* h, int* w) {
 
 int tk_net_is_fused(const tk_net* net) { return net ? net->fused : -1; }
 
+// diagnostics: per-CTA timestamps of the last conv launched with
+// TK_CONV_DBG & 16 (148 x 8 u64, globaltimer ns)
+int tk_debug_conv_stamps(unsigned long long* host_out) {
+  return cudaMemcpyFromSymbol(host_out, g_stamps, sizeof(unsigned long long) * 148 * 8) == cudaSuccess &&
+                 cudaMemcpyFromSymbol(host_out + 148 * 8, g_trace, sizeof(unsigned long long) * 5 * 32) ==
+                     cudaSuccess
+             ? TK_OK
+             : TK_ERR_CUDA;
+}
+
 int tk_net_launches(const tk_net* net, int with_out, int with_pooled) {
   if (!net) return -1;
   int n = 0;
@@ -942,22 +1102,16 @@ int tk_net_forward(tk_context* ctx, tk_net* net, const float* x, float* out, flo
   if (net->fused) {
     PackIn pk = net->pack;
     pk.x = x;
-    const size_t sm = (size_t)pk.C * (pk.W + 1) * 4;
-    if (sm > 48 * 1024) cudaFuncSetAttribute(k_pack_input, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k_pack_input<<<net->batch * pk.H, 256, sm, s>>>(pk);
+    const long long total = (long long)pk.N * (pk.C / 16) * pk.H * pk.W;
+    k_pack_input<<<(unsigned)std::min<long long>((total + 255) / 256, 148 * 64), 256, 0, s>>>(pk);
     if (cudaGetLastError() != cudaSuccess) return TK_ERR_CUDA;
     for (const auto& cvs : net->convs)
       for (const auto& cv : cvs)
-        if (run_conv(cv, s) != cudaSuccess) return TK_ERR_CUDA;
+        if (run_conv(cv, x, s) != cudaSuccess) return TK_ERR_CUDA;
     const F32T& f = net->f32[net->final_f];
-    if (out) {
-      const long long total = (long long)net->batch * f.C * f.H * f.W;
-      k_unpack_f32<<<(unsigned)std::min<long long>((total + 255) / 256, 148 * 32), 256, 0, s>>>(
-          f.p, f.pos, net->batch, f.C, f.H, f.W, f.Hp, f.Wp, out);
-    }
+    if (out) cudaMemcpyAsync(out, f.p, (size_t)f.elems * 4, cudaMemcpyDeviceToDevice, s);
     if (pooled)
-      k_pool_f32<<<(net->batch * f.C + 255) / 256, 256, 0, s>>>(f.p, f.pos, net->batch, f.C, f.H, f.W, f.Hp, f.Wp,
-                                                                   pooled);
+      k_pool_nchw<<<(net->batch * f.C + 255) / 256, 256, 0, s>>>(f.p, net->batch * f.C, f.H * f.W, pooled);
     return cudaGetLastError() == cudaSuccess ? TK_OK : TK_ERR_CUDA;
   }
   // generic: NCHW floats through conv2d_ternary (R:linalg.hpp:301-328)
