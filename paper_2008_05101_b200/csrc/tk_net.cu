@@ -97,7 +97,7 @@ __device__ unsigned long long g_stamps[148 * 8];
 // CTA 0 event trace (dbg & 16): [role][item] for the first 32 items
 // role 0 producer after h_empty wait, 1 MMA after a_empty wait, 2 MMA after
 // h_full wait, 3 epilogue group after a_full wait, 4 epilogue done
-__device__ unsigned long long g_trace[5 * 32];
+__device__ unsigned long long g_trace[8 * 32];
 __device__ __forceinline__ unsigned long long gtime() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -248,9 +248,11 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
     const bool do_mma = !(p.dbg & 1);
     int hs_i = 0, h_round = 0, ws_i = 0, w_round = 0, acc = 0, a_round = 0, it = 0;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
+      if (stamp && lane == 0 && blockIdx.x == 0 && it < 32) g_trace[6 * 32 + it] = clock64();
       if (a_round) sm100::mbar_wait(&a_empty[acc], (a_round - 1) & 1);
       if (stamp && lane == 0 && blockIdx.x == 0 && it < 32) g_trace[1 * 32 + it] = clock64();
       sm100::tc_fence_after();
+      if (stamp && lane == 0 && blockIdx.x == 0 && it < 32) g_trace[7 * 32 + it] = clock64();
       const uint32_t d = tmem + acc * BN;
       int ch = rot_c;
       for (int ci = 0; ci < p.chunks; ++ci) {
@@ -290,6 +292,7 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
         if (++ch == p.chunks) ch = 0;
       }
       sm100::mma_commit_elect(&a_full[acc]);
+      if (stamp && lane == 0 && blockIdx.x == 0 && it < 32) g_trace[5 * 32 + it] = clock64();
       if (++acc == kAcc) { acc = 0; ++a_round; }
     }
     if (stamp && lane == 0) g_stamps[blockIdx.x * 8 + 3] = gtime();
@@ -1078,7 +1081,7 @@ int tk_net_is_fused(const tk_net* net) { return net ? net->fused : -1; }
 // TK_CONV_DBG & 16 (148 x 8 u64, globaltimer ns)
 int tk_debug_conv_stamps(unsigned long long* host_out) {
   return cudaMemcpyFromSymbol(host_out, g_stamps, sizeof(unsigned long long) * 148 * 8) == cudaSuccess &&
-                 cudaMemcpyFromSymbol(host_out + 148 * 8, g_trace, sizeof(unsigned long long) * 5 * 32) ==
+                 cudaMemcpyFromSymbol(host_out + 148 * 8, g_trace, sizeof(unsigned long long) * 8 * 32) ==
                      cudaSuccess
              ? TK_OK
              : TK_ERR_CUDA;

@@ -24,17 +24,18 @@ def main():
     for _ in range(3):
         body.forward(x, check_errors=False)
     torch.cuda.synchronize()
-    st = np.zeros(148 * 8 + 5 * 32, np.uint64)
+    st = np.zeros(148 * 8 + 8 * 32, np.uint64)
     L = _lib.lib()
     L.tk_debug_conv_stamps.argtypes = [C.c_void_p]
     assert L.tk_debug_conv_stamps(st.ctypes.data) == 0
-    tr = st[148 * 8:].reshape(5, 32).astype(np.int64)
+    tr = st[148 * 8:].reshape(8, 32).astype(np.int64)
     s = st[:148 * 8].reshape(148, 8).astype(np.int64)
-    base = s[0, 0]
-    print("CTA0 trace (us): item: prod_after_empty, mma_after_aempty, mma_after_hfull, epi_after_afull, "
-          "mma_after_taps")
-    for i in range(12):
-        print(i, " ".join(f"{(tr[r, i] - base) / 1000:8.2f}" if tr[r, i] else "    -   " for r in range(5)))
+    base = tr[tr > 0].min()
+    cols = [(6, "mma_top"), (1, "after_aempty"), (7, "after_fence"), (2, "after_hfull"), (4, "after_taps"),
+            (5, "after_commits"), (0, "producer"), (3, "epi_afull")]
+    print("CTA0 trace, SM clocks: " + " ".join(f"{n:>12s}" for _, n in cols))
+    for i in range(10):
+        print(f"{i:2d} " + " ".join(f"{tr[r, i] - base:12d}" if tr[r, i] else f"{'-':>12s}" for r, _ in cols))
     t0 = s[:, 0].min()
     rel = (s[:, :6] - t0) / 1000.0
     names = ["start", "mma_setup", "w_res_ready", "mma_done", "epi_done", "end"]
