@@ -2,23 +2,25 @@
 """Benchmark of the FATNN ternary hot path on B200 (contract: one JSON line).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload resnet18|resnet50|fc|conv|dot]
+                    [--workload resnet18|resnet50|fc]
 
 Metric (BASELINE.json): "ternary GEMM Tops/s & ResNet-18 img/s vs roofline at
-1/2/4/8 B200".  The default workload is ResNet-18 ternary inference at batch
-256 per GPU (cfg4; images sharded over GPUs with no collective -> weak
-scaling); `--workload fc` measures the cfg3 4096x4096 FC GEMM in Tops/s.
+1/2/4/8 B200".  The default workload is cfg4, ResNet-18 ternary inference at
+batch 256 per GPU (images sharded over ranks with no collective on the hot
+path -> weak scaling); `--workload fc` measures cfg3 (FC 4096x4096, batch
+256) in Tops/s, `--workload resnet50` cfg5 (batch 128 per GPU by default).
 
-* value   -- units/s with inputs resident in HBM (device CUDA-event time per
-             step, L2 flushed between steps, max over ranks).
-* e2e     -- the same metric through the public API with host buffers: pinned
-             H2D of the step's input and D2H of its result inside the timed
-             region.
-* roofline-- the dominant kernel's algorithmic work per launch / its average
-             launch time (CUDA events on its stream), against the measured
-             peak of its pipe (profiles/peaks_r01.json).
-* cpu_baseline -- the reference's own CPU implementation (oracle/_ref, the
-             unmodified headers) on this host, on a bounded sample.
+* value    -- units/s with inputs resident in HBM: device time of one step
+              (CUDA-graph replay of the ternary path), L2 flushed between
+              steps, max over ranks.
+* e2e      -- the same metric through the public API with host buffers:
+              pinned H2D of the step's input, the full call (float stem ->
+              ternary body -> float head for ResNets) and D2H of its result.
+* roofline -- the dominant kernel's algorithmic work per launch / its
+              device time (CUDA events on its stream), against the measured
+              peak of its pipe (profiles/peaks_r01.json).
+* cpu_baseline -- the reference's own CPU code (oracle/_ref: the unmodified
+              headers compiled from /root/reference) on this host, bounded sample.
 `--impl reference` times that same reference CPU implementation on all host
 threads for the same workload and prints the line with "impl": "reference".
 """
@@ -31,7 +33,6 @@ import statistics
 import subprocess
 import sys
 import threading
-import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
@@ -84,7 +85,7 @@ class ClockSampler:
                     self.rows.append([c.strip() for c in out.split(",")])
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.1)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -110,7 +111,7 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(self.rows)}
 
 
-def dist_setup(n_gpus: int):
+def dist_setup():
     import torch
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -151,13 +152,27 @@ class L2Flush:
         self.buf.fill_(1.0)
 
 
+def graph_of(fn):
+    """Capture fn() (one step of the ternary path) in a CUDA graph."""
+    import torch
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        fn()  # warm the allocator / lazy init outside capture
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        fn()
+    torch.cuda.synchronize()
+    return g
+
+
 # ---------------------------------------------------------------------------
-# workloads (ours)
+# workloads
 
 class FcWorkload:
-    """cfg3: ternary FC 4096x4096, batch 256: quantize+pack -> GEMM -> folded BN."""
-
-    name = "fc"
+    """cfg3: ternary FC 4096x4096, batch 256: quantize -> GEMM -> folded BN."""
 
     def __init__(self, batch=256, cin=4096, cout=4096, seed=0):
         import numpy as np
@@ -176,12 +191,16 @@ class FcWorkload:
         self.x = torch.from_numpy(self.x_host).cuda()
         self.x_pin = torch.from_numpy(self.x_host).pin_memory()
         self.y_pin = torch.empty((batch, cout), dtype=torch.float32).pin_memory()
+        self.y = torch.empty((batch, cout), dtype=torch.float32, device="cuda")
         self.x_dev2 = torch.empty_like(self.x)
+        self.a8 = tk.quantize_levels(self.x, tk.QuantThresholds(0.5, 0.9), tk.QuantMode.kActivationNonneg,
+                                     tk.layer_k_pad(self.layer))
         self.units_per_step = 2.0 * batch * cin * cout / 1e12  # Tera-ops
         self.unit = "Tops/s"
         self.launches_per_step = 2
         self.config = {"workload": "cfg3 ternary FC 4096x4096 batch 256 (quantize+pack -> GEMM -> folded BN)",
-                       "batch": batch, "in": cin, "out": cout, "backend": "auto",
+                       "batch": batch, "in": cin, "out": cout,
+                       "backend": self.layer.backend_for(batch).name,
                        "l2": "flushed between steps (256 MB write)"}
 
     def step(self):
@@ -196,16 +215,24 @@ class FcWorkload:
     def e2e_bytes(self):
         return self.x_host.nbytes, self.B * self.N * 4
 
-    def dominant(self):
-        """(description, algorithmic work per launch, unit, bound, launcher)."""
-        tk = self.tk
-        layer = self.layer
-        be = layer.backend_for(self.B)
-        rows = tk.quantize_and_pack_rows(self.x, tk.QuantThresholds(0.5, 0.9), tk.QuantMode.kActivationNonneg)
-        buf = tk.Im2colBuffer(rows, rows.shape[1], self.B, self.C, True, self.B, 1, 1)
-        flops = 2.0 * self.B * self.C * self.N
-        return (f"ternary GEMM ({be.name})", flops / 1e12, "TFLOP/s", "tensor" if be == tk.Backend.TC_I8 else "int",
-                lambda: tk.packed_gemm(buf, layer), be)
+    def roofline(self, flush) -> dict:
+        """Dominant kernel: the tensor-core GEMM (tk_gemm_levels), CUDA events."""
+        import torch
+        g = graph_of(lambda: self.tk.gemm_levels(self.a8, self.layer, fused=True, out=self.y))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        tot, n = 0.0, 20
+        for _ in range(n):
+            flush()
+            e0.record()
+            g.replay()
+            e1.record()
+            e1.synchronize()
+            tot += e0.elapsed_time(e1)
+        ms = tot / n
+        work = 2.0 * self.B * self.C * self.N / 1e12
+        return {"kernel": "ternary GEMM, tcgen05.mma kind::i8 (k_gemm_tc_i8)", "bound": "tensor",
+                "work": work, "unit": "TFLOP/s", "avg_launch_ms": ms,
+                "algorithmic": f"2*M*N*K = {2 * self.B * self.C * self.N:.4g} int8 ops per launch"}
 
     def verify(self):
         import numpy as np
@@ -218,22 +245,25 @@ class FcWorkload:
         return st == 0 and np.array_equal(y[:4].view(np.int32), ref.reshape(4, self.N).view(np.int32))
 
     def cpu_baseline(self, threads: int) -> dict:
-        """The reference (oracle/_ref) on a bounded sample: im2col_quantize_pack +
-        packed_gemm with the reference's worker threads."""
-        import ctypes as C
-        import numpy as np
-        from oracle.oracle import Reference, ptr, _f32p, _i8p
-        R = Reference()
-        rows = 64
-        xs = np.ascontiguousarray(self.x_host[:rows])
-        sec = C.c_double()
-        st = R.lib.ref_time_fc_gemm(ptr(xs, _f32p), rows, self.C, ptr(self.wq, _i8p), self.N, 0.5, 0.9,
-                                    threads, 1, C.byref(sec), None)
-        assert st == 0
-        t = sec.value
-        return {"value": 2.0 * rows * self.C * self.N / t / 1e12, "unit": self.unit, "cores": threads,
-                "kind": "reference", "sample": f"{rows} of {self.B} rows, 1 call (rows are independent)",
-                "seconds": t}
+        return fc_reference(self.x_host, self.wq, threads, rows=64)
+
+
+def fc_reference(x_host, wq, threads, rows=64) -> dict:
+    """The reference (oracle/_ref): im2col_quantize_pack + packed_gemm with the
+    reference's worker threads, on `rows` of the batch (rows are independent)."""
+    import ctypes as C
+    import numpy as np
+    from oracle.oracle import Reference, ptr, _f32p, _i8p
+    R = Reference()
+    xs = np.ascontiguousarray(x_host[:rows])
+    n, k = wq.shape
+    sec = C.c_double()
+    st = R.lib.ref_time_fc_gemm(ptr(xs, _f32p), rows, k, ptr(wq, _i8p), n, 0.5, 0.9, threads, 1,
+                                C.byref(sec), None)
+    assert st == 0
+    return {"value": 2.0 * rows * k * n / sec.value / 1e12, "unit": "Tops/s", "cores": threads,
+            "kind": "reference", "sample": f"{rows} of the batch rows, 1 call of packed_gemm(workers={threads})",
+            "seconds": sec.value}
 
 
 def build_workload(name: str):
@@ -245,34 +275,17 @@ def build_workload(name: str):
     raise SystemExit(f"unknown workload {name}")
 
 
-def time_dominant(w, iters: int = 20) -> tuple[float, str, float, str, str]:
-    import torch
-    desc, work, unit, bound, fn, be = w.dominant()
-    for _ in range(3):
-        fn()
-    flush = L2Flush()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    tot = 0.0
-    for _ in range(iters):
-        flush()
-        e0.record()
-        fn()
-        e1.record()
-        e1.synchronize()
-        tot += e0.elapsed_time(e1)
-    return tot / iters, desc, work, unit, bound
-
-
 def run_ours(args) -> None:
     import torch
-    rank, world, local = dist_setup(args.gpus)
+    rank, world, local = dist_setup()
     w = build_workload(args.workload)
     assert w.verify(), "parity check failed before timing"
     flush = L2Flush()
-    stream = torch.cuda.current_stream()
-    # ---- device-resident timing ----
+    g = graph_of(w.step)
+    # ---- device-resident timing: graph replay of one step, L2 flushed ----
     for _ in range(args.warmup):
-        w.step()
+        flush()
+        g.replay()
     torch.cuda.synchronize()
     barrier(world)
     e0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -282,9 +295,9 @@ def run_ours(args) -> None:
         barrier(world)
         for i in range(args.steps):
             flush()
-            e0[i].record(stream)
-            w.step()
-            e1[i].record(stream)
+            e0[i].record()
+            g.replay()
+            e1[i].record()
         torch.cuda.synchronize()
     barrier(world)
     ms = sum(a.elapsed_time(b) for a, b in zip(e0, e1)) / args.steps
@@ -299,30 +312,34 @@ def run_ours(args) -> None:
     ee1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     for i in range(args.steps):
         flush()
-        ee0[i].record(stream)
+        ee0[i].record()
         w.step_e2e()
-        ee1[i].record(stream)
+        ee1[i].record()
     torch.cuda.synchronize()
     ems = max_over_ranks(sum(a.elapsed_time(b) for a, b in zip(ee0, ee1)) / args.steps, world)
     e2e_value = w.units_per_step * world / (ems / 1e3)
     # ---- roofline of the dominant kernel ----
-    dms, desc, work, unit, bound = time_dominant(w)
+    r = w.roofline(flush)
     peaks = load_peaks()
-    if bound == "tensor":
-        peak, psrc = peaks["i8_tc_tops"], "measured int8 tensor GEMM (profiles/peaks_r01.json)"
-    elif bound == "int":
+    if r["bound"] == "tensor":
+        peak, psrc = peaks["i8_tc_tops"], "measured int8 tensor GEMM, cuBLASLt via torch._int_mm (profiles/peaks_r01.json)"
+    elif r["bound"] == "int":
         peak, psrc = peaks["popc_tops"], "measured POPC pipe x 32 ops (tools/pipe_bench.cu)"
     else:
         peak, psrc = peaks["hbm_gbs"], "MEASURED_PEAKS.json hbm_gbs"
-    achieved = work / (dms / 1e3)
-    roof = {"kernel": desc, "bound": "tensor" if bound == "tensor" else ("int" if bound == "int" else "hbm"),
-            "achieved": round(achieved, 3), "peak": round(peak, 2), "unit": unit,
-            "frac": round(achieved / peak, 4), "traffic": getattr(w, "traffic", None),
-            "peak_source": psrc, "avg_launch_ms": round(dms, 5)}
+    achieved = r["work"] / (r["avg_launch_ms"] / 1e3)
+    roof = {"kernel": r["kernel"], "bound": r["bound"], "achieved": round(achieved, 3), "peak": round(peak, 2),
+            "unit": r["unit"], "frac": round(achieved / peak, 4), "traffic": r.get("traffic"),
+            "peak_source": psrc, "avg_launch_ms": round(r["avg_launch_ms"], 5),
+            "algorithmic": r.get("algorithmic")}
+    for k in ("per_layer", "launches_timed"):
+        if k in r:
+            roof[k] = r[k]
     line = {"metric": METRIC, "value": round(value, 3), "unit": w.unit, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 5),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int8/2-bit ternary",
-            "data": "synthetic (numpy seeded inputs, random ternary weights)", "config": w.config,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "int8 levels / 2-bit ternary codes (f32 folded-BN epilogue)",
+            "data": "synthetic (seeded inputs, random ternary weights, synthetic BN)", "config": w.config,
             "e2e": {"value": round(e2e_value, 3), "unit": w.unit, "ms_per_step": round(ems, 5),
                     "h2d_bytes_per_step": w.e2e_bytes()[0], "d2h_bytes_per_step": w.e2e_bytes()[1]},
             "gpu_launches": w.launches_per_step * args.steps, "roofline": roof,
@@ -348,24 +365,24 @@ def run_reference(args) -> None:
     if args.workload == "fc":
         import numpy as np
         rng = np.random.default_rng(0)
-        w = FcWorkload.__new__(FcWorkload)
-        w.B, w.C, w.N = 256, 4096, 4096
-        w.wq = rng.integers(-1, 2, (w.N, w.C)).astype(np.int8)
-        rng.uniform(0.5, 1.5, w.N); rng.standard_normal(w.N)
-        w.x_host = np.abs(rng.standard_normal((w.B, w.C))).astype(np.float32)
-        w.unit = "Tops/s"
-        w.config = {"workload": "cfg3 ternary FC 4096x4096 batch 256", "batch": 256, "in": 4096, "out": 4096}
+        wq = rng.integers(-1, 2, (4096, 4096)).astype(np.int8)
+        rng.uniform(0.5, 1.5, 4096)
+        rng.standard_normal(4096)
+        x_host = np.abs(rng.standard_normal((256, 4096))).astype(np.float32)
         vals = []
+        cb = None
         for i in range(args.warmup + args.steps):
-            cb = w.cpu_baseline(threads)
+            cb = fc_reference(x_host, wq, threads, rows=64)
             if i >= args.warmup:
                 vals.append(cb["value"])
         v = statistics.mean(vals)
         cb["value"] = v
-        line = {"metric": METRIC, "impl": "reference", "value": round(v, 5), "unit": w.unit, "n_gpus": 0,
-                "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "config": w.config,
-                "cpu_baseline": cb, "e2e": {"value": round(v, 5), "unit": w.unit, "h2d_bytes_per_step": 0,
-                                            "d2h_bytes_per_step": 0}}
+        line = {"metric": METRIC, "impl": "reference", "value": round(v, 5), "unit": "Tops/s", "n_gpus": 0,
+                "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+                "config": {"workload": "cfg3 ternary FC 4096x4096 batch 256", "batch": 256, "in": 4096,
+                           "out": 4096},
+                "cpu_baseline": cb,
+                "e2e": {"value": round(v, 5), "unit": "Tops/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     else:
         from paper_2008_05101_b200.resnet import reference_cpu_run
         line = reference_cpu_run(args, METRIC, threads)

@@ -204,6 +204,14 @@ int tk_net_forward(tk_context* ctx, tk_net* net, const float* x, float* out,
                    float* pooled, void* stream);
 /* number of kernel launches one tk_net_forward issues */
 int tk_net_launches(const tk_net* net, int with_out, int with_pooled);
+/* diagnostics: per-conv device time of the last forward after
+ * tk_net_set_timing(net, 1) (fused path), and MACs per conv (whole batch) */
+int tk_net_num_convs(const tk_net* net);
+int tk_net_set_timing(tk_net* net, int on);
+int tk_net_conv_times(tk_net* net, float* ms_host, double* macs_host);
+/* diagnostics: per-CTA phase stamps of the last conv run with TK_CONV_DBG&16
+ * (148*8 + 8*32 u64) */
+int tk_debug_conv_stamps(unsigned long long* host_out);
 
 #ifdef __cplusplus
 }

@@ -68,6 +68,10 @@ SIGNATURES = {
     "tk_net_is_fused": (_i, [_vp]),
     "tk_net_forward": (_i, [_vp, _vp, _vp, _vp, _vp, _vp]),
     "tk_net_launches": (_i, [_vp, _i, _i]),
+    "tk_net_num_convs": (_i, [_vp]),
+    "tk_net_set_timing": (_i, [_vp, _i]),
+    "tk_net_conv_times": (_i, [_vp, _vp, _vp]),
+    "tk_debug_conv_stamps": (_i, [_vp]),
 }
 
 TK_NET_AUTO = 0

@@ -606,6 +606,9 @@ struct tk_net {
   PackIn pack{};
   int final_f = -1;
   std::vector<float*> gbuf;  // generic path buffers
+  // optional per-conv timing (tk_net_set_timing): events around each conv
+  int timing = 0;
+  std::vector<cudaEvent_t> ev;
   size_t gbuf_elems = 0;
 };
 
@@ -1058,11 +1061,13 @@ int tk_net_destroy(tk_net* net) {
   for (auto& cvs : net->convs)
     for (auto& cv : cvs) {
       cudaFree(cv.d_w); cudaFree(cv.d_gain); cudaFree(cv.d_bias); cudaFree(cv.d_ithr);
+      (void)0;
       if (cv.layer) tk_layer_destroy(cv.layer);
     }
   for (auto& t : net->s8) cudaFree(t.p);
   for (auto& f : net->f32) cudaFree(f.p);
   for (auto* p : net->gbuf) cudaFree(p);
+  for (auto e : net->ev) cudaEventDestroy(e);
   delete net;
   return TK_OK;
 }
@@ -1099,6 +1104,44 @@ int tk_net_launches(const tk_net* net, int with_out, int with_pooled) {
   return n + (with_out ? 1 : 0) + (with_pooled ? 1 : 0);
 }
 
+int tk_net_num_convs(const tk_net* net) {
+  if (!net) return -1;
+  int n = 0;
+  for (const auto& cvs : net->convs) n += (int)cvs.size();
+  return n;
+}
+
+// Per-conv device timing of subsequent forwards (fused path): events are
+// recorded around every conv launch on the forward's stream.
+int tk_net_set_timing(tk_net* net, int on) {
+  if (!net) return TK_ERR_INVALID;
+  if (on && net->ev.empty()) {
+    net->ev.resize(2 * tk_net_num_convs(net));
+    for (auto& e : net->ev)
+      if (cudaEventCreate(&e) != cudaSuccess) return TK_ERR_CUDA;
+  }
+  net->timing = on && net->fused;
+  return TK_OK;
+}
+
+// ms of each conv of the LAST timed forward (synchronises on its events);
+// also fills MACs per conv (whole batch) when macs != NULL.
+int tk_net_conv_times(tk_net* net, float* ms, double* macs) {
+  if (!net || !net->timing) return TK_ERR_INVALID;
+  int ci = 0;
+  for (const auto& cvs : net->convs)
+    for (const auto& cv : cvs) {
+      if (ms) {
+        if (cudaEventSynchronize(net->ev[2 * ci + 1]) != cudaSuccess) return TK_ERR_CUDA;
+        cudaEventElapsedTime(&ms[ci], net->ev[2 * ci], net->ev[2 * ci + 1]);
+      }
+      if (macs)
+        macs[ci] = (double)net->batch * cv.k.Ho * cv.k.Wo * cv.d.out_c * cv.d.in_c * cv.d.k * cv.d.k;
+      ++ci;
+    }
+  return TK_OK;
+}
+
 int tk_net_forward(tk_context* ctx, tk_net* net, const float* x, float* out, float* pooled, void* stream) {
   if (!ctx || !net || !x) return TK_ERR_INVALID;
   cudaStream_t s = (cudaStream_t)stream;
@@ -1108,9 +1151,14 @@ int tk_net_forward(tk_context* ctx, tk_net* net, const float* x, float* out, flo
     const long long total = (long long)pk.N * (pk.C / 16) * pk.H * pk.W;
     k_pack_input<<<(unsigned)std::min<long long>((total + 255) / 256, 148 * 64), 256, 0, s>>>(pk);
     if (cudaGetLastError() != cudaSuccess) return TK_ERR_CUDA;
+    int ci = 0;
     for (const auto& cvs : net->convs)
-      for (const auto& cv : cvs)
+      for (const auto& cv : cvs) {
+        if (net->timing) cudaEventRecord(net->ev[2 * ci], s);
         if (run_conv(cv, x, s) != cudaSuccess) return TK_ERR_CUDA;
+        if (net->timing) cudaEventRecord(net->ev[2 * ci + 1], s);
+        ++ci;
+      }
     const F32T& f = net->f32[net->final_f];
     if (out) cudaMemcpyAsync(out, f.p, (size_t)f.elems * 4, cudaMemcpyDeviceToDevice, s);
     if (pooled)

@@ -138,6 +138,23 @@ class TernaryBody:
                 pass
             self._h = None
 
+    def conv_times(self, x: torch.Tensor, flush=None, reps: int = 5):
+        """Per-conv device times (ms, averaged over reps forwards, L2 flushed
+        before each by `flush`) and MACs per conv for the whole batch."""
+        n = T.lib().tk_net_num_convs(self._h)
+        check(T.lib().tk_net_set_timing(self._h, 1), "set_timing")
+        ms = np.zeros(n, np.float32)
+        acc = np.zeros(n, np.float64)
+        macs = np.zeros(n, np.float64)
+        for _ in range(reps):
+            if flush:
+                flush()
+            self.forward(x, check_errors=False)
+            check(T.lib().tk_net_conv_times(self._h, ms.ctypes.data, macs.ctypes.data), "conv_times")
+            acc += ms
+        check(T.lib().tk_net_set_timing(self._h, 0), "set_timing")
+        return acc / reps, macs
+
     def launches(self, with_out=False, with_pooled=True) -> int:
         return T.lib().tk_net_launches(self._h, int(with_out), int(with_pooled))
 
@@ -229,12 +246,19 @@ class ResNetWorkload:
     def e2e_bytes(self):
         return self.images_host.numel() * 4, self.B * 1000 * 4
 
-    def dominant(self):
-        """Dominant kernel: the whole ternary body (its convs are >95% of the
-        step); algorithmic work = 2 x body MACs."""
-        flops = 2.0 * self.macs_per_img * self.B
-        return ("ternary conv body (tcgen05 kind::i8 fused convs)" if self.net.body.fused else
-                "ternary conv body (generic)", flops / 1e12, "TFLOP/s", "tensor", self.step, None)
+    def roofline(self, flush) -> dict:
+        """Dominant kernel: the fused ternary conv (k_conv_tc, one launch per
+        conv layer, >90% of the step).  Achieved = 2 x MACs of all its launches
+        / the summed device time of those launches (CUDA events on the
+        forward's stream, L2 flushed before each forward)."""
+        ms, macs = self.net.body.conv_times(self.x, flush=flush, reps=5)
+        tot_ms = float(ms.sum())
+        per = [{"conv": i, "ms": round(float(m), 4), "gmac": round(float(a) / 1e9, 3),
+                "tops": round(2 * float(a) / (float(m) / 1e3) / 1e12, 1)} for i, (m, a) in enumerate(zip(ms, macs))]
+        return {"kernel": "fused ternary conv, tcgen05.mma kind::i8 (k_conv_tc), all conv launches of a step",
+                "bound": "tensor", "work": 2.0 * float(macs.sum()) / 1e12 / len(ms), "unit": "TFLOP/s",
+                "avg_launch_ms": tot_ms / len(ms), "launches_timed": len(ms), "per_layer": per,
+                "algorithmic": f"2 x {float(macs.sum()) / 1e9:.1f} GMAC per step over {len(ms)} launches"}
 
     def verify(self) -> bool:
         """Body parity on a 2-image subsample vs the C oracle (bit-exact f32)."""
