@@ -2,13 +2,15 @@
 """Benchmark of the FATNN ternary hot path on B200 (contract: one JSON line).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload resnet18|resnet50|fc]
+                    [--workload resnet18|resnet50|fc|conv|dot]
 
 Metric (BASELINE.json): "ternary GEMM Tops/s & ResNet-18 img/s vs roofline at
 1/2/4/8 B200".  The default workload is cfg4, ResNet-18 ternary inference at
 batch 256 per GPU (images sharded over ranks with no collective on the hot
 path -> weak scaling); `--workload fc` measures cfg3 (FC 4096x4096, batch
-256) in Tops/s, `--workload resnet50` cfg5 (batch 128 per GPU by default).
+256) in Tops/s, `--workload resnet50` cfg5 (global batch 1024 sharded over
+the ranks -> strong scaling), `--workload conv` cfg2 (one 3x3 conv 64->64,
+56x56, b1) and `--workload dot` cfg1 (65,536 ternary inner products, N=4096).
 
 * value    -- units/s with inputs resident in HBM: device time of one step
               (CUDA-graph replay of the ternary path), L2 flushed between
@@ -33,6 +35,8 @@ import statistics
 import subprocess
 import sys
 import threading
+
+import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
@@ -266,19 +270,225 @@ def fc_reference(x_host, wq, threads, rows=64) -> dict:
             "seconds": sec.value}
 
 
-def build_workload(name: str):
+def _time_graph(g, flush, n=20) -> float:
+    """Mean device ms of one replay of CUDA graph g (events on the current
+    stream, which is the stream the captured kernels run on), L2 flushed."""
+    import torch
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    tot = 0.0
+    for _ in range(n):
+        flush()
+        e0.record()
+        g.replay()
+        e1.record()
+        e1.synchronize()
+        tot += e0.elapsed_time(e1)
+    return tot / n
+
+
+class DotWorkload:
+    """cfg1: fast ternary inner product, N=4096, P=65,536 independent pairs
+    (SURVEY §8(d)): x = pack(|N(0,1)| @ (0.5, 0.9), nonneg), y = pack(N(0,1)
+    @ (0.8, 1.2), weight), result ternary_dot_nonneg(x, y, w_sum) -- the
+    LOP3+POPC kernel k_dot_batched, HBM-bound (2,056 algorithmic B/pair)."""
+
+    def __init__(self, pairs=65536, n=4096, seed=0):
+        import torch
+        from paper_2008_05101_b200 import ternkit as tk
+        self.tk, self.P, self.N = tk, pairs, n
+        g = torch.Generator(device="cuda").manual_seed(seed)
+        xf = torch.randn((pairs, n), generator=g, device="cuda").abs_()
+        yf = torch.randn((pairs, n), generator=g, device="cuda")
+        self.x = tk.quantize_and_pack_rows(xf, tk.QuantThresholds(0.5, 0.9), tk.QuantMode.kActivationNonneg)
+        self.y = tk.quantize_and_pack_rows(yf, tk.QuantThresholds(0.8, 1.2), tk.QuantMode.kWeight)
+        # w_sum = sum of the weight levels = popcount(codes) - lanes (+ padding cancels)
+        self.wsum = self._wsum_host(self.y.cpu().numpy().view(np.uint64), n)
+        self.wsum_dev = torch.from_numpy(self.wsum).cuda()
+        self.xf_sample = xf[:64].cpu().numpy()
+        self.yf_sample = yf[:64].cpu().numpy()
+        del xf, yf
+        self.x_host = self.x.cpu().pin_memory()
+        self.y_host = self.y.cpu().pin_memory()
+        self.wsum_host = self.wsum_dev.cpu().pin_memory()
+        self.x2, self.y2, self.w2 = torch.empty_like(self.x), torch.empty_like(self.y), torch.empty_like(self.wsum_dev)
+        self.out_host = torch.empty(pairs, dtype=torch.int64).pin_memory()
+        self.words = self.x.shape[1]
+        self.bytes_per_pair = 2 * self.words * 8 + 8 + 8  # x, y rows + w_sum in + int64 out
+        self.units_per_step = 2.0 * pairs * n / 1e12
+        self.unit = "Tops/s"
+        self.launches_per_step = 1
+        self.config = {"workload": f"cfg1 ternary inner product N={n}, {pairs} packed pairs "
+                                   "(ternary_dot_nonneg, LOP3+POPC)", "n": n, "pairs": pairs,
+                       "alpha_x": [0.5, 0.9], "alpha_y": [0.8, 1.2],
+                       "l2": "flushed between steps (256 MB write); operands 134 MB > L2"}
+
+    @staticmethod
+    def _wsum_host(words_u64, n):
+        pc = np.bitwise_count(words_u64).sum(axis=1, dtype=np.int64)
+        return pc - words_u64.shape[1] * 32  # sum of levels (padding lanes contribute 0)
+
+    def step(self):
+        return self.tk.ternary_dot_batched(self.x, self.y, self.wsum_dev)
+
+    def step_e2e(self):
+        self.x2.copy_(self.x_host, non_blocking=True)
+        self.y2.copy_(self.y_host, non_blocking=True)
+        self.w2.copy_(self.wsum_host, non_blocking=True)
+        r = self.tk.ternary_dot_batched(self.x2, self.y2, self.w2)
+        self.out_host.copy_(r, non_blocking=True)
+        return r
+
+    def e2e_bytes(self):
+        return self.x_host.numel() * 8 * 2 + self.P * 8, self.P * 8
+
+    def roofline(self, flush) -> dict:
+        ms = _time_graph(graph_of(self.step), flush)
+        return {"kernel": "k_dot_batched (LOP3 + POPC, warp per pair)", "bound": "hbm",
+                "work": self.P * self.bytes_per_pair / 1e9, "unit": "GB/s", "avg_launch_ms": ms,
+                "algorithmic": f"{self.bytes_per_pair} B/pair x {self.P} pairs per launch"}
+
+    def verify(self) -> bool:
+        from oracle.oracle import Oracle
+        O = Oracle()
+        ok = True
+        for (xs, ys) in [(self.xf_sample, self.yf_sample)]:
+            st, xw = zip(*[O.quantize_and_pack(r, 0.5, 0.9, 1) for r in xs])
+            st2, yw = zip(*[O.quantize_and_pack(r, 0.8, 1.2, 0) for r in ys])
+            xw, yw = np.stack(xw), np.stack(yw)
+            ok &= np.array_equal(xw, self.x[:64].cpu().numpy().view(np.uint64))
+            ok &= np.array_equal(yw, self.y[:64].cpu().numpy().view(np.uint64))
+            st, want = O.ternary_dot_batched(xw, yw, self.wsum[:64])
+            ok &= st == 0 and np.array_equal(want, self.step()[:64].cpu().numpy())
+        return bool(ok)
+
+    def reference_time(self, threads: int, pairs: int | None = None):
+        from oracle.oracle import Reference
+        R = Reference()
+        p = pairs or self.P
+        xh = self.x_host[:p].numpy().view(np.uint64)
+        yh = self.y_host[:p].numpy().view(np.uint64)
+        st, out, sec = R.time_dot(xh, yh, self.N, self.wsum[:p], threads)
+        assert st == 0
+        return 2.0 * p * self.N / sec / 1e12, sec, p
+
+    def cpu_baseline(self, threads: int) -> dict:
+        v, sec, p = self.reference_time(threads)
+        return {"value": v, "unit": "Tops/s", "cores": threads, "kind": "reference",
+                "sample": f"all {p} pairs, ternary_dot_nonneg over {threads} host threads (oracle/_ref)",
+                "seconds": sec}
+
+
+class ConvWorkload:
+    """cfg2: one ternary 3x3 conv 64->64, 56x56, batch 1 through
+    conv2d_ternary (R:linalg.hpp:301-328): pack-fused im2col -> ternary GEMM
+    -> folded BN.  Inputs follow the reference bench recipe
+    (R:include/ternkit/bench.hpp:229-255): x ~ |N(0,1)|, weights U{-1,0,1},
+    thr_w (1,1), thr_a (0.5,0.5), random BN folded by fuse_bn.  The GEMM pipe
+    (LOP3+POPC or tcgen05 i8) is chosen by timing both on this shape."""
+
+    def __init__(self, batch=1, c=64, hw=56, seed=0):
+        import torch
+        from paper_2008_05101_b200 import ternkit as tk
+        self.tk = tk
+        rng = np.random.default_rng(seed)
+        self.shape = tk.TensorShape(batch, c, hw, hw)
+        self.geom = tk.ConvGeometry(c, c, 3, 3, 1, 1)
+        self.wq = rng.integers(-1, 2, (c, 9 * c)).astype(np.int8)
+        aff = tk.fuse_bn(rng.standard_normal(c).astype(np.float32) * 0.1,
+                         rng.uniform(0.5, 1.5, c).astype(np.float32),
+                         rng.uniform(0.5, 1.5, c).astype(np.float32),
+                         rng.standard_normal(c).astype(np.float32) * 0.1, 1e-5)
+        self.layer = tk.make_packed_conv_layer(self.wq, self.geom, tk.QuantThresholds(1.0, 1.0),
+                                               tk.QuantThresholds(0.5, 0.5), True, aff)
+        self.x_host_np = np.abs(rng.standard_normal(self.shape.count())).astype(np.float32)
+        self.x = torch.from_numpy(self.x_host_np).cuda()
+        self.x_host = torch.from_numpy(self.x_host_np).pin_memory()
+        self.x2 = torch.empty_like(self.x)
+        M = batch * hw * hw
+        self.M, self.K, self.Nc = M, 9 * c, c
+        self.y_host = torch.empty((batch, c, hw, hw), dtype=torch.float32).pin_memory()
+        self.units_per_step = 2.0 * M * self.K * self.Nc / 1e12
+        self.unit = "Tops/s"
+        # pipe choice by measurement on this shape
+        self.pipe_ms = {}
+        flush = L2Flush()
+        for be in (tk.Backend.POPC, tk.Backend.TC_I8):
+            self.layer.set_backend(be)
+            self.pipe_ms[be.name] = _time_graph(graph_of(self.step), flush, n=30)
+        best = min(self.pipe_ms, key=self.pipe_ms.get)
+        self.backend = tk.Backend[best]
+        self.layer.set_backend(self.backend)
+        self.launches_per_step = 2 if self.backend == tk.Backend.POPC else 3
+        self.config = {"workload": "cfg2 ternary 3x3 conv 64->64, 56x56, batch 1 (conv2d_ternary: "
+                                   "pack-fused im2col -> ternary GEMM -> folded BN)",
+                       "batch": batch, "in_c": c, "out_c": c, "hw": hw, "gemm_m_n_k": [M, c, 9 * c],
+                       "backend": self.backend.name,
+                       "step_ms_by_backend": {k: round(v, 5) for k, v in self.pipe_ms.items()},
+                       "l2": "flushed between steps (256 MB write)"}
+
+    def step(self):
+        return self.tk.conv2d_ternary(self.x, self.shape, self.layer, check_errors=False).data
+
+    def step_e2e(self):
+        self.x2.copy_(self.x_host, non_blocking=True)
+        y = self.tk.conv2d_ternary(self.x2, self.shape, self.layer, check_errors=False).data
+        self.y_host.copy_(y, non_blocking=True)
+        return y
+
+    def e2e_bytes(self):
+        return self.x_host.numel() * 4, self.y_host.numel() * 4
+
+    def roofline(self, flush) -> dict:
+        """Whole conv2d_ternary step against the chosen pipe (the step is
+        launch-latency bound at b1: 231 Mop is ~0.1 us of tensor-pipe work)."""
+        ms = _time_graph(graph_of(self.step), flush)
+        tk = self.tk
+        bound = "tensor" if self.backend == tk.Backend.TC_I8 else "int"
+        return {"kernel": f"conv2d_ternary step ({self.launches_per_step} launches, {self.backend.name} GEMM)",
+                "bound": bound, "work": self.units_per_step, "unit": "TFLOP/s", "avg_launch_ms": ms,
+                "algorithmic": f"2*M*N*K = {2 * self.M * self.K * self.Nc:.4g} ops per step"}
+
+    def verify(self) -> bool:
+        from oracle.oracle import Oracle
+        O = Oracle()
+        y = self.step().cpu().numpy()
+        st, ref = O.conv2d_ternary(self.x_host_np, self.shape.n, self.shape.c, self.shape.h, self.shape.w,
+                                   self.wq, self.Nc, 3, 1, 1, (0.5, 0.5), True, self.layer.fused.gain,
+                                   self.layer.fused.bias, 1.0)
+        return st == 0 and np.array_equal(y.reshape(-1).view(np.int32), ref.reshape(-1).view(np.int32))
+
+    def spec(self):
+        return dict(in_c=self.shape.c, out_c=self.Nc, k=3, stride=1, pad=1, weights=self.wq, ta=(0.5, 0.5),
+                    tw=(1.0, 1.0), gain=self.layer.fused.gain, bias=self.layer.fused.bias, out_scale=1.0)
+
+    def cpu_baseline(self, threads: int) -> dict:
+        from oracle.oracle import Reference
+        R = Reference()
+        s = self.shape
+        st, _, sec = R.time_conv(self.x_host_np, s.n, s.c, s.h, s.w, self.spec(), threads, iters=20)
+        assert st == 0
+        return {"value": self.units_per_step / sec, "unit": "Tops/s", "cores": threads, "kind": "reference",
+                "sample": f"20 calls of conv2d_ternary(workers={threads}) on the full cfg2 input (oracle/_ref)",
+                "seconds": sec}
+
+
+def build_workload(name: str, rank: int = 0, world: int = 1):
     if name == "fc":
         return FcWorkload()
+    if name == "dot":
+        return DotWorkload()
+    if name == "conv":
+        return ConvWorkload()
     if name in ("resnet18", "resnet50"):
         from paper_2008_05101_b200.resnet import ResNetWorkload
-        return ResNetWorkload(name)
+        return ResNetWorkload(name, rank=rank, world=world)
     raise SystemExit(f"unknown workload {name}")
 
 
 def run_ours(args) -> None:
     import torch
     rank, world, local = dist_setup()
-    w = build_workload(args.workload)
+    w = build_workload(args.workload, rank, world)
     assert w.verify(), "parity check failed before timing"
     flush = L2Flush()
     g = graph_of(w.step)
@@ -302,7 +512,9 @@ def run_ours(args) -> None:
     barrier(world)
     ms = sum(a.elapsed_time(b) for a, b in zip(e0, e1)) / args.steps
     ms = max_over_ranks(ms, world)
-    value = w.units_per_step * world / (ms / 1e3)
+    # units_per_step: whole-job units when the workload shards itself, else per rank
+    job_units = w.units_per_step if getattr(w, "world", 1) == world else w.units_per_step * world
+    value = job_units / (ms / 1e3)
     # ---- end to end through the public API with host buffers ----
     for _ in range(max(1, args.warmup)):
         w.step_e2e()
@@ -317,7 +529,7 @@ def run_ours(args) -> None:
         ee1[i].record()
     torch.cuda.synchronize()
     ems = max_over_ranks(sum(a.elapsed_time(b) for a, b in zip(ee0, ee1)) / args.steps, world)
-    e2e_value = w.units_per_step * world / (ems / 1e3)
+    e2e_value = job_units / (ems / 1e3)
     # ---- roofline of the dominant kernel ----
     r = w.roofline(flush)
     peaks = load_peaks()
@@ -335,13 +547,16 @@ def run_ours(args) -> None:
     for k in ("per_layer", "launches_timed"):
         if k in r:
             roof[k] = r[k]
+    h2d, d2h = w.e2e_bytes()
+    if getattr(w, "world", 1) != world:  # replicated workload: every rank moves its own bytes
+        h2d, d2h = h2d * world, d2h * world
     line = {"metric": METRIC, "value": round(value, 3), "unit": w.unit, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 5),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": getattr(w, "scaling", "weak"), "vs_baseline": None,
             "dtype": "int8 levels / 2-bit ternary codes (f32 folded-BN epilogue)",
             "data": "synthetic (seeded inputs, random ternary weights, synthetic BN)", "config": w.config,
             "e2e": {"value": round(e2e_value, 3), "unit": w.unit, "ms_per_step": round(ems, 5),
-                    "h2d_bytes_per_step": w.e2e_bytes()[0], "d2h_bytes_per_step": w.e2e_bytes()[1]},
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": w.launches_per_step * args.steps, "roofline": roof,
             "clocks": clk.summary()}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -362,7 +577,9 @@ def run_reference(args) -> None:
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built for this host"}))
         return
     threads = os.cpu_count() or 1
-    if args.workload == "fc":
+    if args.workload in ("dot", "conv"):
+        line = reference_small(args, threads)
+    elif args.workload == "fc":
         import numpy as np
         rng = np.random.default_rng(0)
         wq = rng.integers(-1, 2, (4096, 4096)).astype(np.int8)
@@ -387,6 +604,50 @@ def run_reference(args) -> None:
         from paper_2008_05101_b200.resnet import reference_cpu_run
         line = reference_cpu_run(args, METRIC, threads)
     print(json.dumps(line), flush=True)
+
+
+def reference_small(args, threads) -> dict:
+    """--impl reference for cfg1 (dot) / cfg2 (conv): the reference's own CPU
+    code (oracle/_ref) on host-generated inputs of the same shape."""
+    from oracle.oracle import Reference
+    R = Reference()
+    rng = np.random.default_rng(0)
+    vals = []
+    if args.workload == "dot":
+        n, pairs = 4096, 8192
+        xs = np.abs(rng.standard_normal((pairs, n), dtype=np.float32))
+        ys = rng.standard_normal((pairs, n), dtype=np.float32)
+        xw = np.stack([R.quantize_and_pack(r, 0.5, 0.9, 1)[1] for r in xs])
+        yw = np.stack([R.quantize_and_pack(r, 0.8, 1.2, 0)[1] for r in ys])
+        wsum = DotWorkload._wsum_host(yw, n)
+        for i in range(args.warmup + args.steps):
+            st, _, sec = R.time_dot(xw, yw, n, wsum, threads)
+            assert st == 0
+            if i >= args.warmup:
+                vals.append(2.0 * pairs * n / sec / 1e12)
+        sample = f"{pairs} of the 65536 pairs per step, ternary_dot_nonneg over {threads} threads"
+        cfg = {"workload": "cfg1 ternary inner product N=4096 (reference CPU, oracle/_ref)", "n": n,
+               "pairs": 65536}
+    else:
+        c, hw = 64, 56
+        spec = dict(in_c=c, out_c=c, k=3, stride=1, pad=1, weights=rng.integers(-1, 2, (c, 9 * c)).astype(np.int8),
+                    ta=(0.5, 0.5), tw=(1.0, 1.0), gain=rng.uniform(0.5, 1.5, c).astype(np.float32),
+                    bias=rng.standard_normal(c).astype(np.float32), out_scale=1.0)
+        x = np.abs(rng.standard_normal(c * hw * hw)).astype(np.float32)
+        work = 2.0 * hw * hw * 9 * c * c / 1e12
+        for i in range(args.warmup + args.steps):
+            st, _, sec = R.time_conv(x, 1, c, hw, hw, spec, threads, iters=5)
+            assert st == 0
+            if i >= args.warmup:
+                vals.append(work / sec)
+        sample = f"5 calls of conv2d_ternary(workers={threads}) per step on the full cfg2 input"
+        cfg = {"workload": "cfg2 ternary 3x3 conv 64->64 56x56 b1 (reference CPU, oracle/_ref)"}
+    v = statistics.mean(vals)
+    return {"metric": METRIC, "impl": "reference", "value": round(v, 6), "unit": "Tops/s", "n_gpus": 0,
+            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "config": cfg,
+            "cpu_baseline": {"value": round(v, 6), "unit": "Tops/s", "cores": threads, "kind": "reference",
+                             "sample": sample},
+            "e2e": {"value": round(v, 6), "unit": "Tops/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
 def main():

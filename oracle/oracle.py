@@ -306,6 +306,32 @@ class Reference:
         L.ref_net_run.argtypes = [C.c_void_p, _f32p] + [C.c_int] * 5 + [_f32p, C.POINTER(C.c_double)]
         L.ref_time_fc_gemm.argtypes = [_f32p, C.c_int, C.c_int, _i8p, C.c_int, C.c_float, C.c_float,
                                        C.c_int, C.c_int, C.POINTER(C.c_double), _i32p]
+        L.ref_time_dot.argtypes = [_u64p, _u64p, _sz, _sz, _i64p, C.c_int, C.POINTER(C.c_double), _i64p]
+        L.ref_time_conv.argtypes = ([_f32p] + [C.c_int] * 4 + [C.POINTER(NdConv), C.c_int, C.c_int,
+                                    C.POINTER(C.c_double), _f32p])
+
+    def time_dot(self, x, y, lanes, wsum, threads):
+        x = np.ascontiguousarray(x, dtype=np.uint64)
+        y = np.ascontiguousarray(y, dtype=np.uint64)
+        ws = np.ascontiguousarray(wsum, dtype=np.int64)
+        out = np.empty(x.shape[0], np.int64)
+        sec = C.c_double()
+        st = self.lib.ref_time_dot(ptr(x, _u64p), ptr(y, _u64p), lanes, x.shape[0], ptr(ws, _i64p),
+                                   threads, C.byref(sec), ptr(out, _i64p))
+        return st, out, sec.value
+
+    def time_conv(self, x, n, c, h, w, spec, workers, iters=1):
+        keep: list = []
+        cv = make_ndconv(spec, keep)
+        x = np.ascontiguousarray(x, dtype=np.float32)
+        k, s, p = spec["k"], spec["stride"], spec["pad"]
+        oh = (h + 2 * p - k) // s + 1
+        ow = (w + 2 * p - k) // s + 1
+        out = np.empty((n, spec["out_c"], oh, ow), np.float32)
+        sec = C.c_double()
+        st = self.lib.ref_time_conv(ptr(x, _f32p), n, c, h, w, C.byref(cv), workers, iters,
+                                    C.byref(sec), ptr(out, _f32p))
+        return st, out, sec.value
 
     def quantize_weight_value(self, p, a1, a2):
         lv = C.c_int()

@@ -373,4 +373,53 @@ int ref_time_fc_gemm(const float* x, int batch, int in_c, const std::int8_t* wq,
   });
 }
 
+// cfg1 timing: `pairs` ternary_dot_nonneg calls (R:bitkernels.hpp:151-159) on
+// vectors packed once up front, pairs sharded over `threads` host threads
+// (the reference's dot is single-threaded; pairs are independent).
+int ref_time_dot(const std::uint64_t* x, const std::uint64_t* y, std::size_t lanes,
+                 std::size_t pairs, const std::int64_t* wsum, int threads,
+                 double* seconds, std::int64_t* out) {
+  return guard([&] {
+    const std::size_t nw = words_for_lanes(lanes);
+    std::vector<PackedTernaryVector> xs(pairs), ys(pairs);
+    for (std::size_t p = 0; p < pairs; ++p) {
+      xs[p].words.assign(x + p * nw, x + (p + 1) * nw);
+      ys[p].words.assign(y + p * nw, y + (p + 1) * nw);
+      xs[p].logical_len = ys[p].logical_len = lanes;
+      xs[p].nonneg_offset = true;
+    }
+    std::vector<std::int64_t> r(pairs);
+    const int nt = threads > 0 ? threads : 1;
+    auto t0 = std::chrono::steady_clock::now();
+    auto work = [&](int t) {  // contiguous ranges: no false sharing on r[]
+      const std::size_t lo = pairs * t / nt, hi = pairs * (t + 1) / nt;
+      for (std::size_t p = lo; p < hi; ++p) r[p] = ternary_dot_nonneg(xs[p], ys[p], wsum[p]);
+    };
+    std::vector<std::thread> pool;
+    for (int t = 1; t < nt; ++t) pool.emplace_back(work, t);
+    work(0);
+    for (auto& th : pool) th.join();
+    *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (out) std::memcpy(out, r.data(), pairs * 8);
+  });
+}
+
+// cfg2 timing: conv2d_ternary (R:linalg.hpp:301-328) with the reference's own
+// worker threads on a layer built once; seconds per call over `iters`.
+int ref_time_conv(const float* x, int n, int c, int h, int w, const nd_conv* conv,
+                  int workers, int iters, double* seconds_per_call, float* out) {
+  return guard([&] {
+    PackedConvLayer layer = build_layer(*conv);
+    const TensorShape s{n, c, h, w};
+    ConvResult r;
+    auto t0 = std::chrono::steady_clock::now();
+    for (int i = 0; i < iters; ++i)
+      r = conv2d_ternary(std::span<const float>(x, s.count()), s, layer, MaskMode::kOnTheFly,
+                         workers);
+    *seconds_per_call =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() / iters;
+    if (out) std::memcpy(out, r.data.data(), r.data.size() * 4);
+  });
+}
+
 }  // extern "C"

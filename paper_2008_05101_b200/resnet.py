@@ -210,26 +210,39 @@ class ResNetWorkload:
     protocol: first and last layers excluded); e2e = the whole network from
     host images (pinned H2D) to logits (D2H)."""
 
-    def __init__(self, name: str = "resnet18", batch: int | None = None, seed: int = 0):
+    def __init__(self, name: str = "resnet18", batch: int | None = None, seed: int = 0,
+                 rank: int = 0, world: int = 1):
+        from .shard import ShardedForward, shard_range
         depth = 18 if name == "resnet18" else 50
-        batch = batch or int(os.environ.get("TK_BENCH_BATCH", 256 if depth == 18 else 128))
-        self.name, self.depth, self.B = name, depth, batch
+        if depth == 18:
+            # cfg4: batch 256 per GPU (weak scaling over 1/2/4/8 GPUs)
+            per_gpu = batch or int(os.environ.get("TK_BENCH_BATCH", 256))
+            global_batch, scaling = per_gpu * world, "weak"
+        else:
+            # cfg5: global batch 1024 sharded across the GPUs (strong scaling)
+            global_batch, scaling = batch or int(os.environ.get("TK_BENCH_BATCH", 1024)), "strong"
+        batch = shard_range(global_batch, rank, world).count
+        self.name, self.depth, self.B, self.global_batch = name, depth, batch, global_batch
+        self.rank, self.world, self.scaling = rank, world, scaling
         self.net = TernaryResNet(depth, batch, seed)
-        g = torch.Generator().manual_seed(seed + 1)
+        # per-rank images: a distinct slice of the synthetic global batch
+        g = torch.Generator().manual_seed(seed + 1 + rank)
         self.images_host = torch.rand(batch, 3, 224, 224, generator=g).pin_memory()
         self.images_dev = self.images_host.cuda()
         self.x = self.net.stem(self.images_dev)  # body input, resident
         self.pooled = torch.empty((batch, self.net.body.out_shape[0]), device="cuda")
-        self.logits_host = torch.empty((batch, 1000)).pin_memory()
+        self.logits_host = torch.empty((global_batch if rank == 0 else 0, 1000)).pin_memory()
         self.img_dev2 = torch.empty_like(self.images_dev)
+        self.sharded = ShardedForward(self.net.forward, global_batch, 1000, rank, world)
         self.macs_per_img = body_macs(self.net.blocks)
-        self.units_per_step = float(batch)
+        self.units_per_step = float(global_batch)  # whole job, all ranks
         self.unit = "img/s"
         self.launches_per_step = self.net.body.launches(False, True)
         self.config = {"workload": f"cfg{'4' if depth == 18 else '5'} {name} ternary body, synthetic 224x224 "
-                                   f"images, batch {batch} per GPU (paper protocol: float stem/head excluded "
-                                   f"from value, included in e2e)",
-                       "model": name, "batch_per_gpu": batch, "image": 224,
+                                   f"images, global batch {global_batch} over {world} GPU(s) (paper protocol: "
+                                   f"float stem/head excluded from value, included in e2e)",
+                       "model": name, "global_batch": global_batch, "batch_per_gpu": batch, "image": 224,
+                       "parallelism": f"batch-sharded dp{world}, logits gathered to rank 0",
                        "fused_pipeline": self.net.body.fused,
                        "body_gmac_per_img": round(self.macs_per_img / 1e9, 4),
                        "l2": "flushed between steps (256 MB write)"}
@@ -238,13 +251,17 @@ class ResNetWorkload:
         return self.net.body.forward(self.x, pooled=self.pooled, check_errors=False)
 
     def step_e2e(self):
+        """Host images -> stem -> ternary body -> head on this rank's shard,
+        logits gathered to rank 0 (the only collective) and read back."""
         self.img_dev2.copy_(self.images_host, non_blocking=True)
-        logits = self.net.forward(self.img_dev2)
-        self.logits_host.copy_(logits, non_blocking=True)
+        logits = self.sharded(self.img_dev2)
+        if logits is not None:
+            self.logits_host.copy_(logits, non_blocking=True)
         return logits
 
     def e2e_bytes(self):
-        return self.images_host.numel() * 4, self.B * 1000 * 4
+        """(H2D, D2H) bytes per step, whole job."""
+        return self.global_batch * 3 * 224 * 224 * 4, self.global_batch * 1000 * 4
 
     def roofline(self, flush) -> dict:
         """Dominant kernel: the fused ternary conv (k_conv_tc, one launch per
