@@ -118,8 +118,10 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
   constexpr uint32_t kCols = Acc<BN>::kCols;
   constexpr int kSteps = R / 32;  // MMAs (K = 32) per tap and chunk
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte alignment by pointer arithmetic on the __shared__ array (not
+  // through an integer cast) so derived pointers keep the shared address
+  // space and the epilogue's parameter reads compile to LDS, not generic LD
+  uint8_t* smem = smem_raw + ((1024u - (sm100::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* halo = smem;
   const int halo_stage = p.n_ph * p.HB;
   uint8_t* wreg = halo + p.hs * halo_stage;
@@ -350,17 +352,21 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
 #pragma unroll
           for (int o = 0; o < 2; ++o) {
             if (o >= p.n_q) break;
-            const int* e0 = reinterpret_cast<const int*>(ep) + o * 3 * p.N + n0;
+            // (c0, c1, sign) of 4 channels per 16-byte LDS (broadcast: all
+            // lanes read the same channels)
+            const int4* e0 = reinterpret_cast<const int4*>(ep + o * 3 * p.N + n0);
+            const int n4 = p.N / 4;
             uint32_t w[8];
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
+              const int4 lo = e0[j], hi = e0[n4 + j], sg = e0[2 * n4 + j];
+              const int xs[4] = {(int)r[4 * j] * sg.x, (int)r[4 * j + 1] * sg.y, (int)r[4 * j + 2] * sg.z,
+                                 (int)r[4 * j + 3] * sg.w};
+              const int l0[4] = {lo.x, lo.y, lo.z, lo.w}, l1[4] = {hi.x, hi.y, hi.z, hi.w};
               uint32_t b = 0;
 #pragma unroll
-              for (int i = 0; i < 4; ++i) {
-                const int c = 4 * j + i;
-                const int x = (int)r[c] * e0[2 * p.N + c];
-                b |= ((uint32_t)(x > e0[c]) + (uint32_t)(x > e0[p.N + c])) << (8 * i);
-              }
+              for (int i = 0; i < 4; ++i)
+                b |= ((uint32_t)(xs[i] > l0[i]) + (uint32_t)(xs[i] > l1[i])) << (8 * i);
               w[j] = b;
             }
             const int Rq = p.q_R[o];
@@ -373,12 +379,16 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
           }
           continue;
         }
-        const float* eg = reinterpret_cast<const float*>(ep) + n0;
+        const float4* eg = reinterpret_cast<const float4*>(ep + n0);
+        const int n4 = p.N / 4;
         float v[32];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          // R:linalg.hpp:322-323 (FMA-contracted like the reference build)
-          v[j] = __fmaf_rn(eg[j], __fmul_rn(p.out_scale, (float)(int32_t)r[j]), eg[p.N + j]);
+        for (int j = 0; j < 8; ++j) {
+          const float4 g = eg[j], bb = eg[n4 + j];
+          const float gs[4] = {g.x, g.y, g.z, g.w}, bs[4] = {bb.x, bb.y, bb.z, bb.w};
+#pragma unroll
+          for (int i = 0; i < 4; ++i)  // R:linalg.hpp:322-323 (FMA-contracted like the reference build)
+            v[4 * j + i] = __fmaf_rn(gs[i], __fmul_rn(p.out_scale, (float)(int32_t)r[4 * j + i]), bs[i]);
         }
         if (p.skip) {  // NCHW: lanes = consecutive positions -> coalesced per channel
           const float* s = p.skip + fbase + (long long)n0 * oplane;
@@ -866,7 +876,10 @@ int setup_fused(tk_net* net) {
       const int wbytes_all = cv.chunks * k.n_taps * k.WB;
       k.resident = (cv.n_tiles == 1 && 2 * halo_stage + wbytes_all <= budget) ? 1 : 0;
       const int wmin = k.resident ? wbytes_all : 3 * k.WB;
-      k.hs = std::max(1, std::min(4, (budget - wmin) / halo_stage));
+      // halo ring depth: enough stages in flight to cover the TMA latency
+      // (env TK_CONV_HS caps it for experiments)
+      const int hs_cap = getenv("TK_CONV_HS") ? std::max(1, atoi(getenv("TK_CONV_HS"))) : 8;
+      k.hs = std::max(1, std::min(hs_cap, (budget - wmin) / halo_stage));
       k.ws = k.resident ? 1 : std::max(2, std::min(8, (budget - k.hs * halo_stage) / k.WB));
       const int wregion = k.resident ? wbytes_all : k.ws * k.WB;
       // epilogue parameter words: at most 2 quantized outputs x 3 ints per channel
