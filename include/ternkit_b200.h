@@ -143,15 +143,20 @@ int tk_conv2d_ternary(tk_context* ctx, const tk_layer* layer, const float* x,
                       int n, int h, int w, int mask_mode, float* out,
                       void* stream);
 
-/* Ternary GEMM on operands already expanded to quantization levels (s8,
- * [m_rows][layer k_pad], zero-padded past the patch length): the contraction
- * packed_gemm performs, without the pack/expand step.  out_mode 0: int32
+/* Ternary GEMM on operands already expanded to quantization levels: the
+ * contraction packed_gemm performs, without the pack/expand step.  a_s8 is
+ * the s8 level operand in K-block-major layout [k_pad/128][m_pad][128]
+ * (m_pad = m_rows rounded up to 128; element (r, k) at
+ * ((k/128)*m_pad + r)*128 + k%128), as tk_quantize_levels writes it, so that
+ * every tensor-core tile load is one contiguous block.  out_mode 0: int32
  * [m_rows][out_c] accumulators; 1: f32 rows after the folded-BN epilogue.
- * Uses the layer's backend choice (tensor cores for TC_I8/AUTO). */
+ * Tensor-core path only (TK_ERR_UNSUPPORTED otherwise). */
 int tk_gemm_levels(tk_context* ctx, const tk_layer* layer, const int8_t* a_s8,
                    int m_rows, int out_mode, void* out, void* stream);
-/* Quantize f32 rows to s8 levels for tk_gemm_levels (activation levels
- * {0,1,2} in nonneg mode, {-1,0,1} in weight mode), zero padded to k_pad. */
+/* Quantize f32 rows [rows][n] to s8 levels for tk_gemm_levels (activation
+ * levels {0,1,2} in nonneg mode, {-1,0,1} in weight mode), zero padded to
+ * k_pad (a multiple of 128), written K-block-major (see tk_gemm_levels):
+ * out holds round_up(rows, 128) * k_pad bytes. */
 int tk_quantize_levels(tk_context* ctx, const float* x, int rows, int n,
                        float alpha1, float alpha2, int mode, int k_pad,
                        int8_t* out, void* stream);
@@ -212,6 +217,9 @@ int tk_net_conv_times(tk_net* net, float* ms_host, double* macs_host);
 /* diagnostics: per-CTA phase stamps of the last conv run with TK_CONV_DBG&16
  * (148*8 + 8*32 u64) */
 int tk_debug_conv_stamps(unsigned long long* host_out);
+/* profiling: per-CTA globaltimer stamps of the last tensor-core GEMM launched
+ * with env TK_GEMM_DBG & 16 (grid-linear CTA id < 512, 8 u64 each) */
+int tk_debug_gemm_stamps(unsigned long long* host_out);
 
 #ifdef __cplusplus
 }

@@ -72,6 +72,7 @@ SIGNATURES = {
     "tk_net_set_timing": (_i, [_vp, _i]),
     "tk_net_conv_times": (_i, [_vp, _vp, _vp]),
     "tk_debug_conv_stamps": (_i, [_vp]),
+    "tk_debug_gemm_stamps": (_i, [_vp]),
 }
 
 TK_NET_AUTO = 0

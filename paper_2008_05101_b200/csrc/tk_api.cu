@@ -83,6 +83,17 @@ void* tk_workspace(tk_context* ctx, size_t bytes) {
   return ctx->ws;
 }
 
+void* tk_red_workspace(tk_context* ctx, size_t bytes) {
+  if (bytes <= ctx->red_bytes) return ctx->red_ws;
+  cudaDeviceSynchronize();
+  if (ctx->red_ws) cudaFree(ctx->red_ws);
+  ctx->red_ws = nullptr;
+  ctx->red_bytes = 0;
+  if (cudaMalloc(&ctx->red_ws, bytes) != cudaSuccess) return nullptr;
+  ctx->red_bytes = bytes;
+  return ctx->red_ws;
+}
+
 extern "C" {
 
 int tk_version(void) { return 100; }
@@ -147,6 +158,7 @@ int tk_context_destroy(tk_context* ctx) {
   if (!ctx) return TK_OK;
   cudaDeviceSynchronize();
   if (ctx->ws) cudaFree(ctx->ws);
+  if (ctx->red_ws) cudaFree(ctx->red_ws);
   if (ctx->d_err) cudaFree(ctx->d_err);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   delete ctx;
@@ -251,7 +263,7 @@ int tk_layer_create(tk_context* ctx, const int8_t* weights_host, int in_c,
       uint64_t& wd = words[(size_t)o * wpr + l / 32];
       wd = (wd & ~(3ull << (2 * (l % 32)))) | (code << (2 * (l % 32)));
       s += v;
-      w8[(size_t)o * k_pad + l] = (int8_t)v;
+      w8[((size_t)(l / 128) * n_pad + o) * 128 + l % 128] = (int8_t)v;  // [k/128][n_pad][128]
     }
     wsum[o] = s;
     int32_t z = 0;
@@ -432,7 +444,7 @@ int tk_gemm_levels(tk_context* ctx, const tk_layer* L, const int8_t* a_s8, int m
 
 int tk_quantize_levels(tk_context* ctx, const float* x, int rows, int n, float a1, float a2,
                        int mode, int k_pad, int8_t* out, void* stream) {
-  if (!ctx || rows < 0 || n < 0 || k_pad < n || k_pad % 16) return TK_ERR_INVALID;
+  if (!ctx || rows < 0 || n < 0 || k_pad < n || k_pad % 128) return TK_ERR_INVALID;
   tk_qparams q;
   const int st = tk_make_qparams(a1, a2, mode, &q);
   if (st != TK_OK) return st;

@@ -149,7 +149,7 @@ __device__ __forceinline__ uint32_t expand4(uint32_t bits8, uint32_t tbl) {
 // integer MMA result equals packed_gemm's offset-corrected dot directly.
 __global__ void k_expand_rows_s8(const uint32_t* __restrict__ rows,
                                  size_t row_count, int w32pr, int offset,
-                                 int k_pad, int8_t* __restrict__ out) {
+                                 int k_pad, size_t m_pad, int8_t* __restrict__ out) {
   const int chunks = k_pad / 16;
   const uint32_t tbl = offset ? 0x02010100u : 0x010000FFu;
   const size_t total = row_count * (size_t)chunks;
@@ -165,14 +165,15 @@ __global__ void k_expand_rows_s8(const uint32_t* __restrict__ rows,
       o.z = expand4((wd >> 16) & 0xFF, tbl);
       o.w = expand4(wd >> 24, tbl);
     }
-    reinterpret_cast<uint4*>(out + r * (size_t)k_pad)[j] = o;
+    // K-block-major operand layout [k/128][m_pad][128] (contiguous TMA boxes)
+    reinterpret_cast<uint4*>(out + ((size_t)(j >> 3) * m_pad + r) * 128)[j & 7] = o;
   }
 }
 
 // Floats -> s8 quantization levels ({0,1,2} activation, {-1,0,1} weight
 // mode) for the tensor-core FC path; columns >= n are zero.
 __global__ void k_quantize_s8(const float* __restrict__ x, size_t rows,
-                              size_t n, tk_qparams q, int k_pad,
+                              size_t n, tk_qparams q, int k_pad, size_t m_pad,
                               int8_t* __restrict__ out,
                               unsigned long long* err, bool vec4) {
   const int chunks = k_pad / 16;
@@ -215,7 +216,8 @@ __global__ void k_quantize_s8(const float* __restrict__ x, size_t rows,
       }
     }
     if (first_bad >= 0) tk_raise(err, r * n + l0 + first_bad, bad_code);
-    reinterpret_cast<uint4*>(out + r * (size_t)k_pad)[j] =
+    // K-block-major operand layout [k/128][m_pad][128] (contiguous TMA boxes)
+    reinterpret_cast<uint4*>(out + ((size_t)(j >> 3) * m_pad + r) * 128)[j & 7] =
         make_uint4(b[0], b[1], b[2], b[3]);
   }
 }
@@ -280,7 +282,7 @@ cudaError_t tk_launch_expand_rows_s8(const uint64_t* rows, size_t row_count,
   if (total == 0) return cudaSuccess;
   k_expand_rows_s8<<<grid_for(total), kThreads, 0, s>>>(
       reinterpret_cast<const uint32_t*>(rows), row_count, 2 * wpr64, offset,
-      k_pad, out);
+      k_pad, (row_count + 127) / 128 * 128, out);
   return cudaGetLastError();
 }
 
@@ -290,7 +292,7 @@ cudaError_t tk_launch_quantize_s8(const float* x, size_t rows, size_t n,
   const size_t total = rows * (size_t)(k_pad / 16);
   if (total == 0) return cudaSuccess;
   const bool vec4 = (n % 4 == 0) && ((uintptr_t)x % 16 == 0);
-  k_quantize_s8<<<grid_for(total), kThreads, 0, s>>>(x, rows, n, q, k_pad, out,
-                                                    err, vec4);
+  k_quantize_s8<<<grid_for(total), kThreads, 0, s>>>(x, rows, n, q, k_pad, (rows + 127) / 128 * 128,
+                                                    out, err, vec4);
   return cudaGetLastError();
 }

@@ -49,11 +49,12 @@ struct ConvK {
   int n_ph;
   int ph_id[4];
   int halo_rows;
+  int hbox, nbox;  // halo rows per TMA box, boxes per halo (a box spans <= 256 rows)
   int chunks;
   long long in_pos;  // rows per phase plane of the input tensor
   int in_phases;
   int base_shift;
-  int n_tiles, m_tiles;
+  int n_tiles, m_tiles, m_items;  // m_items = ceil(m_tiles / MT)
   long long m_total;
   int PHg, PWg, Ho, Wo;
   int hs, ws, resident;
@@ -104,18 +105,20 @@ __device__ __forceinline__ unsigned long long gtime() {
   return t;
 }
 
-template <int BN>
+// MT = 128-row M tiles per work item (they share every weight block and the
+// per-item pipeline overhead); each accumulator buffer holds MT x BN columns
+template <int BN, int MT>
 struct Acc {
-  static constexpr int kN = BN <= 128 ? 4 : 2;  // accumulator buffers
-  static constexpr uint32_t kCols = kN * BN;    // TMEM columns (power of 2)
+  static constexpr int kN = BN * MT <= 128 ? 4 : 2;  // accumulator buffers
+  static constexpr uint32_t kCols = kN * BN * MT;    // TMEM columns (power of 2)
 };
 
-template <int BN, int R, int KT>
+template <int BN, int R, int KT, int MT>
 __global__ void __launch_bounds__(kConvThreads, 1)
 k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CUtensorMap w_map,
           const ConvK p) {
-  constexpr int kAcc = Acc<BN>::kN;
-  constexpr uint32_t kCols = Acc<BN>::kCols;
+  constexpr int kAcc = Acc<BN, MT>::kN;
+  constexpr uint32_t kCols = Acc<BN, MT>::kCols;
   constexpr int kSteps = R / 32;  // MMAs (K = 32) per tap and chunk
   extern __shared__ uint8_t smem_raw[];
   // 1024-byte alignment by pointer arithmetic on the __shared__ array (not
@@ -162,7 +165,7 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
     }
     for (int s = 0; s < kAcc; ++s) {
       sm100::mbar_init(&a_full[s], 1);
-      sm100::mbar_init(&a_empty[s], kEpiThreads / 2);  // one epilogue group per tile
+      sm100::mbar_init(&a_empty[s], kEpiThreads / 2 * MT);  // one epilogue group per M tile
     }
     sm100::mbar_init(w_res, 1);
 #pragma unroll
@@ -176,7 +179,7 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
   __syncthreads();
   sm100::tc_fence_after();
   const uint32_t tmem = *tslot;
-  const int n_items = p.m_tiles * p.n_tiles;
+  const int n_items = p.m_items * p.n_tiles;
   // CTAs walk the (chunk, tap) weight blocks from different starting points
   // (integer sums are order independent) so they do not all hit the same L2
   // lines at once.
@@ -197,7 +200,7 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
     int mt = blockIdx.x / p.n_tiles, nt = blockIdx.x - mt * p.n_tiles;
     const int dmt = gridDim.x / p.n_tiles, dnt = gridDim.x - dmt * p.n_tiles;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-      const int row0 = mt * 128 + p.base_shift;
+      const int row0 = mt * (MT * 128) + p.base_shift;
       int ch = rot_c;
       for (int ci = 0; ci < p.chunks; ++ci) {
         if (h_round) sm100::mbar_wait(&h_empty[hs_i], (h_round - 1) & 1);
@@ -207,11 +210,12 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
           if (p.dbg & 2) {
             sm100::mbar_arrive(&h_full[hs_i]);
           } else {
-            sm100::mbar_arrive_expect_tx(&h_full[hs_i], (uint32_t)(p.n_ph * p.halo_rows * R));
+            sm100::mbar_arrive_expect_tx(&h_full[hs_i], (uint32_t)(p.n_ph * p.nbox * p.hbox * R));
             const long long rbase = (long long)ch * p.in_phases * p.in_pos + row0;
             for (int s2 = 0; s2 < p.n_ph; ++s2)
-              sm100::tma_load_2d(halo + hs_i * halo_stage + s2 * p.HB, &in_map, &h_full[hs_i], 0,
-                                 (int)(rbase + (long long)s_ph[s2] * p.in_pos));
+              for (int b = 0; b < p.nbox; ++b)
+                sm100::tma_load_2d(halo + hs_i * halo_stage + s2 * p.HB + b * p.hbox * R, &in_map, &h_full[hs_i],
+                                   0, (int)(rbase + (long long)s_ph[s2] * p.in_pos + b * p.hbox));
           }
         }
         __syncwarp();
@@ -255,7 +259,7 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
       if (stamp && lane == 0 && blockIdx.x == 0 && it < 32) g_trace[1 * 32 + it] = clock64();
       sm100::tc_fence_after();
       if (stamp && lane == 0 && blockIdx.x == 0 && it < 32) g_trace[7 * 32 + it] = clock64();
-      const uint32_t d = tmem + acc * BN;
+      const uint32_t d = tmem + acc * (BN * MT);
       int ch = rot_c;
       for (int ci = 0; ci < p.chunks; ++ci) {
         sm100::mbar_wait(&h_full[hs_i], h_round & 1);
@@ -278,9 +282,11 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
           if (do_mma) {
 #pragma unroll
             for (int k = 0; k < kSteps; ++k)
-              sm100::mma_i8_elect(d, tmpl | (uint64_t)(((ab + k * 32) & 0x3FFFFu) >> 4),
-                                  tmpl | (uint64_t)(((wb + k * 32) & 0x3FFFFu) >> 4), idesc,
-                                  (ci | t | k) != 0);
+#pragma unroll
+              for (int u = 0; u < MT; ++u)
+                sm100::mma_i8_elect(d + u * BN, tmpl | (uint64_t)(((ab + u * 128 * R + k * 32) & 0x3FFFFu) >> 4),
+                                    tmpl | (uint64_t)(((wb + k * 32) & 0x3FFFFu) >> 4), idesc,
+                                    (ci | t | k) != 0);
           }
           if (!p.resident) {
             sm100::mma_commit_elect(&w_empty[ws_i]);
@@ -315,8 +321,12 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
     const uint32_t* ep = eparam;
     int it = 0;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
-      if ((it & 1) != grp) continue;
-      const int mt = item / p.n_tiles, nt = item - mt * p.n_tiles;
+      // MT == 1: the two groups take alternate items; MT == 2: group g takes
+      // M tile g of every item
+      if (MT == 1 && (it & 1) != grp) continue;
+      const int mi = item / p.n_tiles, nt = item - mi * p.n_tiles;
+      const int mt = mi * MT + (MT == 1 ? 0 : grp);
+      const uint32_t tcol = (uint32_t)(it % kAcc) * (BN * MT) + (MT == 1 ? 0 : grp * BN);
       const int acc = it % kAcc;
       if (p.dbg & 8) {  // profiling: bare accumulator hand-off
         if (!(p.dbg & 64) || lane == 0) sm100::mbar_wait(&a_full[acc], (it / kAcc) & 1);
@@ -338,12 +348,22 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
       const int ph4 = (py & 1) * 2 + (px & 1);
       // NCHW index of (img, channel 0, oy, ox) in the f32 skip / output tensors
       const long long fbase = (long long)img * p.N * oplane + (long long)oy * p.Wo + ox;
+      // skip values are independent of the accumulator: the first chunk's
+      // loads are issued before waiting for the MMAs, each later chunk's
+      // while the previous one is finished (HBM latency off the critical path)
+      const bool pre = p.skip && valid && !(p.dbg & 4);
+      const float* skp = p.skip + fbase + (long long)(nt * BN) * oplane;
+      float sk[32];
+      if (pre) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) sk[j] = __ldg(skp + j * oplane);
+      }
       sm100::mbar_wait(&a_full[acc], (it / kAcc) & 1);
       sm100::tc_fence_after();
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 32) {
         uint32_t r[32];
-        sm100::tmem_ld32(tmem + ((uint32_t)(qtr * 32) << 16) + acc * BN + c0, r);
+        sm100::tmem_ld32(tmem + ((uint32_t)(qtr * 32) << 16) + tcol + c0, r);
         sm100::tmem_ld_wait();
         if (!valid || (p.dbg & 4)) continue;
         const int n0 = nt * BN + c0;
@@ -390,10 +410,14 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
           for (int i = 0; i < 4; ++i)  // R:linalg.hpp:322-323 (FMA-contracted like the reference build)
             v[4 * j + i] = __fmaf_rn(gs[i], __fmul_rn(p.out_scale, (float)(int32_t)r[4 * j + i]), bs[i]);
         }
-        if (p.skip) {  // NCHW: lanes = consecutive positions -> coalesced per channel
-          const float* s = p.skip + fbase + (long long)n0 * oplane;
+        if (pre) {  // NCHW: lanes = consecutive positions -> coalesced per channel
 #pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] += __ldg(s + j * oplane);
+          for (int j = 0; j < 32; ++j) v[j] += sk[j];
+          if (c0 + 32 < BN) {
+            const float* s = skp + (long long)(c0 + 32) * oplane;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) sk[j] = __ldg(s + j * oplane);
+          }
         }
         if (p.relu) {
 #pragma unroll
@@ -600,6 +624,7 @@ struct Conv {
   CUtensorMap in_map{}, w_map{};
   int smem = 0;
   int grid = 0;
+  int MT = 1;  // 128-row M tiles per work item
 };
 
 }  // namespace
@@ -691,7 +716,7 @@ void plan_taps(Conv& cv, const S8T& in) {
     k.tap_slot[i] = slot_of[phs[i]];
     k.tap_shift[i] = shifts[i] - mn;
   }
-  k.halo_rows = (128 + (mx - mn) + 7) / 8 * 8;
+  k.halo_rows = mx - mn;  // tap span; the halo size is set once MT is chosen
   k.in_phases = in.phases;
   k.in_pos = in.pos;
   k.chunks = in.C / in.R;
@@ -858,8 +883,10 @@ int setup_fused(tk_net* net) {
   for (auto& f : net->f32)
     if (cudaMalloc(&f.p, (size_t)f.elems * 4) != cudaSuccess) return TK_ERR_CUDA;
   // per-conv kernel parameters
+  int conv_no = -1;
   for (auto& cvs : net->convs)
     for (auto& cv : cvs) {
+      ++conv_no;
       const S8T& in = net->s8[cv.in_idx];
       int st = prepare_conv_weights(cv, in.R);
       if (st != TK_OK) return st;
@@ -869,6 +896,21 @@ int setup_fused(tk_net* net) {
       k.m_total = (long long)net->batch * k.PHg * k.PWg;
       k.m_tiles = (int)((k.m_total + 127) / 128);
       if (k.m_total + 1024 > (1ll << 31)) return TK_ERR_UNSUPPORTED;  // 32-bit row indices
+      // two M tiles per item where the accumulators fit TMEM twice over
+      // (BN <= 128); env TK_CONV_MT=1 forces one (experiments)
+      cv.MT = (cv.BN <= 128 && k.m_tiles > 1) ? 2 : 1;
+      if (getenv("TK_CONV_MT")) cv.MT = std::min(cv.MT, std::max(1, atoi(getenv("TK_CONV_MT"))));
+      k.m_items = (k.m_tiles + cv.MT - 1) / cv.MT;
+      {
+        const int span = k.halo_rows;
+        const int rows = (cv.MT * 128 + span + 7) / 8 * 8;
+        k.nbox = (rows + 255) / 256;
+        // box starts stay 1024-byte aligned in SMEM (the swizzle atom period)
+        const int align = 1024 / cv.R;
+        k.hbox = ((rows + k.nbox - 1) / k.nbox + align - 1) / align * align;
+        if (k.hbox > 256) { ++k.nbox; k.hbox = ((rows + k.nbox - 1) / k.nbox + align - 1) / align * align; }
+        k.halo_rows = k.nbox * k.hbox;
+      }
       k.HB = (k.halo_rows * cv.R + 1023) / 1024 * 1024;
       k.WB = (cv.BN * cv.R + 1023) / 1024 * 1024;
       const int budget = 224 * 1024 - 6 * cv.d.out_c * 4 - 1536;  // of 227 KB dynamic SMEM
@@ -930,9 +972,11 @@ int setup_fused(tk_net* net) {
       }
       k.err = net->ctx->d_err;
       k.dbg = getenv("TK_CONV_DBG") ? atoi(getenv("TK_CONV_DBG")) : 0;
-      if (!map_rows(&cv.in_map, in.p, (unsigned long long)(in.C / in.R) * in.phases * in.pos, in.R, k.halo_rows))
+      // profiling: TK_CONV_DBG_ONLY=<launch order index> limits the knob to one conv
+      if (getenv("TK_CONV_DBG_ONLY") && atoi(getenv("TK_CONV_DBG_ONLY")) != conv_no) k.dbg = 0;
+      if (!map_rows(&cv.in_map, in.p, (unsigned long long)(in.C / in.R) * in.phases * in.pos, in.R, k.hbox))
         return TK_ERR_CUDA;
-      const int items = k.m_tiles * k.n_tiles;
+      const int items = k.m_items * k.n_tiles;
       cv.grid = std::min(items, net->ctx->num_sms);
       if (getenv("TK_CONV_GRID")) cv.grid = std::min(items, atoi(getenv("TK_CONV_GRID")));  // profiling
     }
@@ -956,30 +1000,38 @@ int setup_fused(tk_net* net) {
   return TK_OK;
 }
 
-template <int BN, int R, int KT>
+template <int BN, int R, int KT, int MT>
 cudaError_t launch_conv(const Conv& cv, const float* x, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
     // 227 KB per block, less the kernel's static shared tables
-    cudaFuncSetAttribute(k_conv_tc<BN, R, KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024);
+    cudaFuncSetAttribute(k_conv_tc<BN, R, KT, MT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024);
     attr = true;
   }
   ConvK k = cv.k;
   if (cv.skip_f == -2) k.skip = x;  // identity shortcut = the forward's input
-  k_conv_tc<BN, R, KT><<<cv.grid, kConvThreads, cv.smem, s>>>(cv.in_map, cv.w_map, k);
+  k_conv_tc<BN, R, KT, MT><<<cv.grid, kConvThreads, cv.smem, s>>>(cv.in_map, cv.w_map, k);
   return cudaGetLastError();
+}
+
+template <int BN, int R, int KT>
+cudaError_t launch_conv_mt(const Conv& cv, const float* x, cudaStream_t s) {
+  if constexpr (BN <= 128) {
+    if (cv.MT == 2) return launch_conv<BN, R, KT, 2>(cv, x, s);
+  }
+  return launch_conv<BN, R, KT, 1>(cv, x, s);
 }
 
 template <int KT>
 cudaError_t run_conv_kt(const Conv& cv, const float* x, cudaStream_t s) {
   if (cv.R == 64) {
-    if (cv.BN == 64) return launch_conv<64, 64, KT>(cv, x, s);
-    if (cv.BN == 128) return launch_conv<128, 64, KT>(cv, x, s);
-    return launch_conv<256, 64, KT>(cv, x, s);
+    if (cv.BN == 64) return launch_conv_mt<64, 64, KT>(cv, x, s);
+    if (cv.BN == 128) return launch_conv_mt<128, 64, KT>(cv, x, s);
+    return launch_conv_mt<256, 64, KT>(cv, x, s);
   }
-  if (cv.BN == 64) return launch_conv<64, 128, KT>(cv, x, s);
-  if (cv.BN == 128) return launch_conv<128, 128, KT>(cv, x, s);
-  return launch_conv<256, 128, KT>(cv, x, s);
+  if (cv.BN == 64) return launch_conv_mt<64, 128, KT>(cv, x, s);
+  if (cv.BN == 128) return launch_conv_mt<128, 128, KT>(cv, x, s);
+  return launch_conv_mt<256, 128, KT>(cv, x, s);
 }
 
 cudaError_t run_conv(const Conv& cv, const float* x, cudaStream_t s) {

@@ -501,24 +501,37 @@ def fully_connected_ternary(x, batch: int, layer: PackedConvLayer,
 # level-operand entry points (tensor-core path without the 2-bit pack step)
 
 
-def quantize_levels(x, t: QuantThresholds, mode: QuantMode, k_pad: int) -> torch.Tensor:
-    """f32 [rows][n] -> s8 quantization levels [rows][k_pad] (zero padded)."""
+class LevelOperand:
+    """s8 quantization levels of `rows` rows in the tensor-core operand layout
+    (K-block-major [k_pad/128][m_pad][128], see include/ternkit_b200.h)."""
+
+    def __init__(self, data: torch.Tensor, rows: int, k_pad: int):
+        self.data, self.rows, self.k_pad = data, rows, k_pad
+
+    def dense(self) -> torch.Tensor:
+        """[rows][k_pad] view (a copy), for inspection and tests."""
+        return self.data.permute(1, 0, 2).reshape(-1, self.k_pad)[: self.rows]
+
+
+def quantize_levels(x, t: QuantThresholds, mode: QuantMode, k_pad: int) -> LevelOperand:
+    """f32 [rows][n] -> s8 quantization levels (zero padded to k_pad)."""
     xd = _dev(x, torch.float32)
     rows, n = xd.shape
-    out = torch.empty((rows, k_pad), dtype=torch.int8, device="cuda")
+    m_pad = (rows + 127) // 128 * 128
+    out = torch.zeros((k_pad // 128, m_pad, 128), dtype=torch.int8, device="cuda")
     check(T.lib().tk_quantize_levels(context(), _p(xd), rows, n, t.alpha1, t.alpha2, int(mode), k_pad,
                                      _p(out), _stream()), "quantize_levels")
-    return out
+    return LevelOperand(out, rows, k_pad)
 
 
-def gemm_levels(a_s8: torch.Tensor, layer: PackedConvLayer, fused: bool = False,
+def gemm_levels(a: LevelOperand, layer: PackedConvLayer, fused: bool = False,
                 out: torch.Tensor | None = None) -> torch.Tensor:
     """Ternary GEMM on s8 level operands: int32 accumulators, or (fused=True)
     f32 rows after the folded-BN epilogue."""
-    m = a_s8.shape[0]
+    m = a.rows
     if out is None:
         out = torch.empty((m, layer.geom.out_c), dtype=torch.float32 if fused else torch.int32, device="cuda")
-    check(T.lib().tk_gemm_levels(context(), layer.handle, _p(a_s8), m, 1 if fused else 0, _p(out),
+    check(T.lib().tk_gemm_levels(context(), layer.handle, _p(a.data), m, 1 if fused else 0, _p(out),
                                  _stream()), "gemm_levels")
     return out
 

@@ -190,3 +190,30 @@ def test_fc_cfg3_full_size(tk, oracle, backend):
                                     layer.fused.gain, layer.fused.bias, 1.0)
     assert st == 0
     assert np.array_equal(y[rows].view(np.int32), ref.reshape(xs.shape[0], N).view(np.int32))
+
+
+@pytest.mark.parametrize("rows,k,n", [(256, 4096, 4096), (200, 640, 96), (1, 128, 8), (300, 1280, 260)])
+def test_level_operand_gemm(tk, oracle, rows, k, n):
+    """quantize_levels -> gemm_levels (the cfg3 kernels on their own): levels
+    equal the oracle quantizer, int32 accumulators equal the integer matmul,
+    across split-K cluster sizes (ragged rows / columns included)."""
+    rng = np.random.default_rng(rows + k + n)
+    wq = rng.integers(-1, 2, (n, k)).astype(np.int8)
+    layer = _layer(tk, wq, k, n, 1, 1, 0)
+    x = np.abs(rng.standard_normal((rows, k))).astype(np.float32)
+    a = tk.quantize_levels(torch.from_numpy(x).cuda(), tk.QuantThresholds(0.5, 0.9), tk.QuantMode.kActivationNonneg,
+                           tk.layer_k_pad(layer))
+    lv = a.dense().cpu().numpy()[:, :k].astype(np.int64)
+    st, words = oracle.quantize_and_pack(x[: min(rows, 8)].reshape(-1), 0.5, 0.9, 1)
+    want_lv = oracle.unpack(words, min(rows, 8) * k).reshape(min(rows, 8), k).astype(np.int64) + 1
+    assert np.array_equal(lv[: min(rows, 8)], want_lv)
+    want = lv @ wq.T.astype(np.int64)
+    got = tk.gemm_levels(a, layer).cpu().numpy()
+    assert np.array_equal(got, want)
+    gain = rng.uniform(0.5, 1.5, n).astype(np.float32)
+    bias = rng.standard_normal(n).astype(np.float32)
+    layer2 = _layer(tk, wq, k, n, 1, 1, 0, gain=gain, bias=bias)
+    y = tk.gemm_levels(a, layer2, fused=True).cpu().numpy()
+    r4 = min(rows, 4)  # fmaf epilogue: the oracle's conv epilogue on the same inputs
+    st, yo = oracle.conv2d_ternary(x[:r4], r4, k, 1, 1, wq, n, 1, 1, 0, (0.5, 0.9), True, gain, bias, 1.0)
+    assert st == 0 and np.array_equal(y[:r4].view(np.int32), yo.reshape(r4, n).view(np.int32))

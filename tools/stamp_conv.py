@@ -18,7 +18,11 @@ def main():
     hw = int(os.environ.get("HW", 56))
     batch = int(os.environ.get("B", 256))
     rng = np.random.default_rng(0)
-    blocks = [dict(convs=[_conv(rng, c, c, 3, 1, (0.5, 0.9), False)])]
+    if os.environ.get("INNER"):  # trace the inner (integer-threshold epilogue) conv of a 2-conv block
+        os.environ["TK_CONV_DBG_ONLY"] = "0"
+        blocks = [dict(convs=[_conv(rng, c, c, 3, 1, (0.5, 0.9)), _conv(rng, c, c, 3, 1, (0.45, 0.85), False)])]
+    else:
+        blocks = [dict(convs=[_conv(rng, c, c, 3, 1, (0.5, 0.9), False)])]
     body = TernaryBody(blocks, batch, c, hw, hw)
     x = torch.relu(torch.randn(batch, c, hw, hw, device="cuda"))
     for _ in range(3):
@@ -34,7 +38,7 @@ def main():
     cols = [(6, "mma_top"), (1, "after_aempty"), (7, "after_fence"), (2, "after_hfull"), (4, "after_taps"),
             (5, "after_commits"), (0, "producer"), (3, "epi_afull")]
     print("CTA0 trace, SM clocks: " + " ".join(f"{n:>12s}" for _, n in cols))
-    for i in range(10):
+    for i in range(int(os.environ.get('ROWS', 10))):
         print(f"{i:2d} " + " ".join(f"{tr[r, i] - base:12d}" if tr[r, i] else f"{'-':>12s}" for r, _ in cols))
     t0 = s[:, 0].min()
     rel = (s[:, :6] - t0) / 1000.0
