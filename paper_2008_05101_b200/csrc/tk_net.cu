@@ -74,6 +74,7 @@ struct ConvK {
   float t0[2], t1[2];
   int q_phases[2], q_R[2];
   long long q_pos[2];
+  int q_same;  // both quantized outputs use the same thresholds (levels computed once)
   unsigned long long* err;
   int dbg;  // profiling knob (env TK_CONV_DBG): 1 no MMA, 2 no halo TMA, 4 no epilogue
 };
@@ -353,10 +354,12 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
       // while the previous one is finished (HBM latency off the critical path)
       const bool pre = p.skip && valid && !(p.dbg & 4);
       const float* skp = p.skip + fbase + (long long)(nt * BN) * oplane;
+      const uint32_t ostride = (uint32_t)oplane;  // 32 channel planes < 2^31 elements
       float sk[32];
       if (pre) {
+        uint32_t off = 0;
 #pragma unroll
-        for (int j = 0; j < 32; ++j) sk[j] = __ldg(skp + j * oplane);
+        for (int j = 0; j < 32; ++j, off += ostride) sk[j] = __ldg(skp + off);
       }
       sm100::mbar_wait(&a_full[acc], (it / kAcc) & 1);
       sm100::tc_fence_after();
@@ -402,21 +405,33 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
         const float4* eg = reinterpret_cast<const float4*>(ep + n0);
         const int n4 = p.N / 4;
         float v[32];
+        if (p.out_scale == 1.0f) {  // fmul(1, x) == x exactly: one FMA per value
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const float4 g = eg[j], bb = eg[n4 + j];
-          const float gs[4] = {g.x, g.y, g.z, g.w}, bs[4] = {bb.x, bb.y, bb.z, bb.w};
+          for (int j = 0; j < 8; ++j) {
+            const float4 g = eg[j], bb = eg[n4 + j];
+            const float gs[4] = {g.x, g.y, g.z, g.w}, bs[4] = {bb.x, bb.y, bb.z, bb.w};
 #pragma unroll
-          for (int i = 0; i < 4; ++i)  // R:linalg.hpp:322-323 (FMA-contracted like the reference build)
-            v[4 * j + i] = __fmaf_rn(gs[i], __fmul_rn(p.out_scale, (float)(int32_t)r[4 * j + i]), bs[i]);
+            for (int i = 0; i < 4; ++i)  // R:linalg.hpp:322-323 (FMA-contracted like the reference build)
+              v[4 * j + i] = __fmaf_rn(gs[i], (float)(int32_t)r[4 * j + i], bs[i]);
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const float4 g = eg[j], bb = eg[n4 + j];
+            const float gs[4] = {g.x, g.y, g.z, g.w}, bs[4] = {bb.x, bb.y, bb.z, bb.w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              v[4 * j + i] = __fmaf_rn(gs[i], __fmul_rn(p.out_scale, (float)(int32_t)r[4 * j + i]), bs[i]);
+          }
         }
         if (pre) {  // NCHW: lanes = consecutive positions -> coalesced per channel
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] += sk[j];
           if (c0 + 32 < BN) {
-            const float* s = skp + (long long)(c0 + 32) * oplane;
+            const float* sb = skp + (size_t)(c0 + 32) * ostride;
+            uint32_t off = 0;
 #pragma unroll
-            for (int j = 0; j < 32; ++j) sk[j] = __ldg(s + j * oplane);
+            for (int j = 0; j < 32; ++j, off += ostride) sk[j] = __ldg(sb + off);
           }
         }
         if (p.relu) {
@@ -424,37 +439,50 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
           for (int j = 0; j < 32; ++j) v[j] = v[j] < 0.0f ? 0.0f : v[j];  // std::max(v, 0.0f)
         }
         if (p.fout) {
-          float* o = p.fout + fbase + (long long)n0 * oplane;
+          float* ob = p.fout + fbase + (long long)n0 * oplane;
+          uint32_t off = 0;
 #pragma unroll
-          for (int j = 0; j < 32; ++j) o[j * oplane] = v[j];
+          for (int j = 0; j < 32; ++j, off += ostride) ob[off] = v[j];
         }
-#pragma unroll
-        for (int o = 0; o < 2; ++o) {
-          if (o >= p.n_q) break;
-          uint32_t w[8];
+        if (p.n_q > 0) {
+          // quantizer input checks (R:quantizer.hpp:37-41,53-55), once per
+          // value: after the ReLU a value is >= 0 (or -0.0) unless NaN
           bool bad = false;
+          if (p.relu) {
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            uint32_t b = 0;
+            for (int j = 0; j < 32; ++j) bad |= !(v[j] <= 3.402823466e38f);
+          } else {
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const float x = v[4 * j + i];
-              bad |= !(x >= 0.0f && x <= 3.402823466e38f);
-              const uint32_t lv = (uint32_t)(x > p.t0[o]) + (uint32_t)(x > p.t1[o]);
-              b |= lv << (8 * i);
-            }
-            w[j] = b;
+            for (int j = 0; j < 32; ++j) bad |= !(v[j] >= 0.0f && v[j] <= 3.402823466e38f);
           }
           if (bad) tk_raise(p.err, (unsigned long long)qrow, TK_ERR_NONFINITE);
-          const int Rq = p.q_R[o];
-          const int chq = n0 / Rq, cq = n0 - chq * Rq;
-          const long long off = p.q_phases[o] == 4 ? ((long long)(chq * 4 + ph4) * p.q_pos[o] + P4) * Rq + cq
-                                                   : ((long long)chq * p.q_pos[o] + P1) * Rq + cq;
-          uint4* dst = reinterpret_cast<uint4*>(p.q[o] + off);
-          dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
-          dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+          uint32_t w[8];
+#pragma unroll
+          for (int o = 0; o < 2; ++o) {
+            if (o >= p.n_q) break;
+            if (o == 0 || !p.q_same) {
+              const float t0 = p.t0[o], t1 = p.t1[o];
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                uint32_t b = 0;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                  const float x = v[4 * j + i];
+                  b += ((x > t0) ? (1u << (8 * i)) : 0u) + ((x > t1) ? (1u << (8 * i)) : 0u);
+                }
+                w[j] = b;
+              }
+            }
+            const int Rq = p.q_R[o];
+            const int chq = n0 / Rq, cq = n0 - chq * Rq;
+            const long long off = p.q_phases[o] == 4 ? ((long long)(chq * 4 + ph4) * p.q_pos[o] + P4) * Rq + cq
+                                                     : ((long long)chq * p.q_pos[o] + P1) * Rq + cq;
+            uint4* dst = reinterpret_cast<uint4*>(p.q[o] + off);
+            dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
+            dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+          }
         }
-      }
+            }
       sm100::tc_fence_before();
       sm100::mbar_arrive(&a_empty[acc]);
     }
@@ -896,9 +924,11 @@ int setup_fused(tk_net* net) {
       k.m_total = (long long)net->batch * k.PHg * k.PWg;
       k.m_tiles = (int)((k.m_total + 127) / 128);
       if (k.m_total + 1024 > (1ll << 31)) return TK_ERR_UNSUPPORTED;  // 32-bit row indices
-      // two M tiles per item where the accumulators fit TMEM twice over
-      // (BN <= 128); env TK_CONV_MT=1 forces one (experiments)
-      cv.MT = (cv.BN <= 128 && k.m_tiles > 1) ? 2 : 1;
+      // two M tiles per item (env TK_CONV_MT=1 forces one, experiments)
+      // (measured: pays off for the 64-channel inner convs; the f32-epilogue
+      // convs and wider layers run faster with the two epilogue groups on
+      // alternate items)
+      cv.MT = (cv.BN == 64 && cv.skip_f == -1 && cv.out_f < 0 && k.m_tiles > 1) ? 2 : 1;
       if (getenv("TK_CONV_MT")) cv.MT = std::min(cv.MT, std::max(1, atoi(getenv("TK_CONV_MT"))));
       k.m_items = (k.m_tiles + cv.MT - 1) / cv.MT;
       {
@@ -949,6 +979,7 @@ int setup_fused(tk_net* net) {
         k.q_pos[k.n_q] = q.pos;
         ++k.n_q;
       }
+      k.q_same = k.n_q == 2 && k.t0[0] == k.t0[1] && k.t1[0] == k.t1[1];
       // integer-threshold epilogue for inner convs (ReLU + quantize only)
       k.ithr = nullptr;
       if (cv.relu && cv.skip_f == -1 && cv.out_f < 0 && k.n_q > 0 && k.t0[0] >= 0.0f) {
@@ -1016,7 +1047,7 @@ cudaError_t launch_conv(const Conv& cv, const float* x, cudaStream_t s) {
 
 template <int BN, int R, int KT>
 cudaError_t launch_conv_mt(const Conv& cv, const float* x, cudaStream_t s) {
-  if constexpr (BN <= 128) {
+  if constexpr (BN == 64) {
     if (cv.MT == 2) return launch_conv<BN, R, KT, 2>(cv, x, s);
   }
   return launch_conv<BN, R, KT, 1>(cv, x, s);

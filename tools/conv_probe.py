@@ -24,8 +24,11 @@ def main():
     for m in modes:
         os.environ["TK_CONV_DBG"] = str(m)
         body = TernaryBody(blocks, batch, 64, 56, 56)
-        ms, macs = body.conv_times(x, flush=lambda: flush.fill_(1.0), reps=5)
-        rows[m] = ms
+        runs = []
+        for _ in range(int(os.environ.get("REPS", 15))):
+            ms, macs = body.conv_times(x, flush=lambda: flush.fill_(1.0), reps=1)
+            runs.append(ms)
+        rows[m] = np.median(np.stack(runs), axis=0)  # per conv, robust to outliers
         del body
     os.environ.pop("TK_CONV_DBG", None)
     print("conv  gmac   " + "  ".join(f"dbg{m:<3d}" for m in modes))
