@@ -39,8 +39,15 @@
 
 namespace {
 
-constexpr int kConvThreads = 320;  // warp0 TMA, warp1 MMA, warps 2-9 epilogue
-constexpr int kEpiThreads = 256;
+// warp 0 TMA, warp 1 MMA, then G epilogue groups of 4 warps (one per TMEM
+// lane quarter).  G = 3 groups take turns on items (MT = 1); with two M tiles
+// per item (MT = 2) group g takes tile g.  Three groups fit because the
+// epilogue walks the accumulator row 16 columns at a time (<= 128 registers).
+// (a group waits on accumulator-buffer parity, so groups <= buffers: with
+// at most one pass of lead no waiter can match a stale phase)
+__host__ __device__ constexpr int conv_groups(int BN, int MT) { return MT == 2 ? 2 : (BN <= 128 ? 3 : 2); }
+__host__ __device__ constexpr int conv_threads(int BN, int MT) { return 64 + 128 * conv_groups(BN, MT); }
+constexpr int CH = 16;  // accumulator columns per epilogue step
 
 struct ConvK {
   int n_taps;
@@ -76,7 +83,8 @@ struct ConvK {
   long long q_pos[2];
   int q_same;  // both quantized outputs use the same thresholds (levels computed once)
   unsigned long long* err;
-  int dbg;  // profiling knob (env TK_CONV_DBG): 1 no MMA, 2 no halo TMA, 4 no epilogue
+  int dbg;  // profiling knob (env TK_CONV_DBG): 1 no MMA, 2 no halo TMA, 4 no epilogue,
+            // float epilogue parts: 128 no quantize, 256 no f32 store, 512 no skip load
 };
 
 __device__ __forceinline__ uint64_t desc_sw(uint32_t saddr, int R) {
@@ -89,8 +97,9 @@ __device__ __forceinline__ uint64_t desc_sw(uint32_t saddr, int R) {
   return d;
 }
 
+template <int kThreads>
 __device__ __forceinline__ void epi_bar() {
-  asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
+  asm volatile("bar.sync 1, %0;" ::"n"(kThreads) : "memory");
 }
 
 // profiling stamps (dbg & 16): per CTA [start, setup done, MMA loop done,
@@ -115,7 +124,7 @@ struct Acc {
 };
 
 template <int BN, int R, int KT, int MT>
-__global__ void __launch_bounds__(kConvThreads, 1)
+__global__ void __launch_bounds__(conv_threads(BN, MT), 1)
 k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CUtensorMap w_map,
           const ConvK p) {
   constexpr int kAcc = Acc<BN, MT>::kN;
@@ -166,7 +175,7 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
     }
     for (int s = 0; s < kAcc; ++s) {
       sm100::mbar_init(&a_full[s], 1);
-      sm100::mbar_init(&a_empty[s], kEpiThreads / 2 * MT);  // one epilogue group per M tile
+      sm100::mbar_init(&a_empty[s], 128 * MT);  // one epilogue group per M tile
     }
     sm100::mbar_init(w_res, 1);
 #pragma unroll
@@ -307,10 +316,12 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
     if (stamp && lane == 0) g_stamps[blockIdx.x * 8 + 3] = gtime();
   } else if (warp >= 2) {
     // ================= epilogue =========================================
-    // two groups of 4 warps take alternate tiles (two tiles in flight hide
-    // the TMEM-load and store latencies); within a group warp w owns TMEM
+    // G groups of 4 warps take turns on items (several items in flight hide
+    // the TMEM-load and memory latencies); within a group warp w owns TMEM
     // lane quarter w % 4 and walks all BN columns.
-    const int et = threadIdx.x - 64;  // 0..255
+    constexpr int G = conv_groups(BN, MT), kEpiThreads = 128 * G;
+    static_assert(G <= kAcc, "epilogue groups must not outnumber accumulator buffers");
+    const int et = threadIdx.x - 64;
     const int qtr = warp & 3;
     const int grp = (warp - 2) >> 2;
     const int plane = p.PHg * p.PWg;
@@ -318,13 +329,12 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
     for (int i = et; i < ewords; i += kEpiThreads)
       eparam[i] = p.ithr ? (uint32_t)__ldg(p.ithr + i)
                          : __float_as_uint(__ldg((i < p.N ? p.gain : p.bias - p.N) + i));
-    epi_bar();
+    epi_bar<kEpiThreads>();
     const uint32_t* ep = eparam;
     int it = 0;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
-      // MT == 1: the two groups take alternate items; MT == 2: group g takes
-      // M tile g of every item
-      if (MT == 1 && (it & 1) != grp) continue;
+      // MT == 1: the groups take turns; MT == 2: group g takes M tile g of every item
+      if (MT == 1 && it % G != grp) continue;
       const int mi = item / p.n_tiles, nt = item - mi * p.n_tiles;
       const int mt = mi * MT + (MT == 1 ? 0 : grp);
       const uint32_t tcol = (uint32_t)(it % kAcc) * (BN * MT) + (MT == 1 ? 0 : grp * BN);
@@ -352,21 +362,21 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
       // skip values are independent of the accumulator: the first chunk's
       // loads are issued before waiting for the MMAs, each later chunk's
       // while the previous one is finished (HBM latency off the critical path)
-      const bool pre = p.skip && valid && !(p.dbg & 4);
+      const bool pre = p.skip && valid && !(p.dbg & (4 | 512));
       const float* skp = p.skip + fbase + (long long)(nt * BN) * oplane;
-      const uint32_t ostride = (uint32_t)oplane;  // 32 channel planes < 2^31 elements
-      float sk[32];
+      const uint32_t ostride = (uint32_t)oplane;  // CH channel planes < 2^31 elements
+      float sk[CH];
       if (pre) {
         uint32_t off = 0;
 #pragma unroll
-        for (int j = 0; j < 32; ++j, off += ostride) sk[j] = __ldg(skp + off);
+        for (int j = 0; j < CH; ++j, off += ostride) sk[j] = __ldg(skp + off);
       }
       sm100::mbar_wait(&a_full[acc], (it / kAcc) & 1);
       sm100::tc_fence_after();
 #pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 32) {
-        uint32_t r[32];
-        sm100::tmem_ld32(tmem + ((uint32_t)(qtr * 32) << 16) + tcol + c0, r);
+      for (int c0 = 0; c0 < BN; c0 += CH) {
+        uint32_t r[CH];
+        sm100::tmem_ld16(tmem + ((uint32_t)(qtr * 32) << 16) + tcol + c0, r);
         sm100::tmem_ld_wait();
         if (!valid || (p.dbg & 4)) continue;
         const int n0 = nt * BN + c0;
@@ -379,9 +389,9 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
             // lanes read the same channels)
             const int4* e0 = reinterpret_cast<const int4*>(ep + o * 3 * p.N + n0);
             const int n4 = p.N / 4;
-            uint32_t w[8];
+            uint32_t w[CH / 4];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
+            for (int j = 0; j < CH / 4; ++j) {
               const int4 lo = e0[j], hi = e0[n4 + j], sg = e0[2 * n4 + j];
               const int xs[4] = {(int)r[4 * j] * sg.x, (int)r[4 * j + 1] * sg.y, (int)r[4 * j + 2] * sg.z,
                                  (int)r[4 * j + 3] * sg.w};
@@ -397,17 +407,17 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
             const long long off = p.q_phases[o] == 4 ? ((long long)(chq * 4 + ph4) * p.q_pos[o] + P4) * Rq + cq
                                                      : ((long long)chq * p.q_pos[o] + P1) * Rq + cq;
             uint4* dst = reinterpret_cast<uint4*>(p.q[o] + off);
-            dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
-            dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+#pragma unroll
+            for (int j = 0; j < CH / 16; ++j) dst[j] = make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
           }
           continue;
         }
         const float4* eg = reinterpret_cast<const float4*>(ep + n0);
         const int n4 = p.N / 4;
-        float v[32];
+        float v[CH];
         if (p.out_scale == 1.0f) {  // fmul(1, x) == x exactly: one FMA per value
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
+          for (int j = 0; j < CH / 4; ++j) {
             const float4 g = eg[j], bb = eg[n4 + j];
             const float gs[4] = {g.x, g.y, g.z, g.w}, bs[4] = {bb.x, bb.y, bb.z, bb.w};
 #pragma unroll
@@ -416,7 +426,7 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
           }
         } else {
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
+          for (int j = 0; j < CH / 4; ++j) {
             const float4 g = eg[j], bb = eg[n4 + j];
             const float gs[4] = {g.x, g.y, g.z, g.w}, bs[4] = {bb.x, bb.y, bb.z, bb.w};
 #pragma unroll
@@ -426,44 +436,44 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
         }
         if (pre) {  // NCHW: lanes = consecutive positions -> coalesced per channel
 #pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] += sk[j];
-          if (c0 + 32 < BN) {
-            const float* sb = skp + (size_t)(c0 + 32) * ostride;
+          for (int j = 0; j < CH; ++j) v[j] += sk[j];
+          if (c0 + CH < BN) {
+            const float* sb = skp + (size_t)(c0 + CH) * ostride;
             uint32_t off = 0;
 #pragma unroll
-            for (int j = 0; j < 32; ++j, off += ostride) sk[j] = __ldg(sb + off);
+            for (int j = 0; j < CH; ++j, off += ostride) sk[j] = __ldg(sb + off);
           }
         }
         if (p.relu) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = v[j] < 0.0f ? 0.0f : v[j];  // std::max(v, 0.0f)
+          for (int j = 0; j < CH; ++j) v[j] = v[j] < 0.0f ? 0.0f : v[j];  // std::max(v, 0.0f)
         }
-        if (p.fout) {
+        if (p.fout && !(p.dbg & 256)) {
           float* ob = p.fout + fbase + (long long)n0 * oplane;
           uint32_t off = 0;
 #pragma unroll
-          for (int j = 0; j < 32; ++j, off += ostride) ob[off] = v[j];
+          for (int j = 0; j < CH; ++j, off += ostride) ob[off] = v[j];
         }
-        if (p.n_q > 0) {
+        if (p.n_q > 0 && !(p.dbg & 128)) {
           // quantizer input checks (R:quantizer.hpp:37-41,53-55), once per
           // value: after the ReLU a value is >= 0 (or -0.0) unless NaN
           bool bad = false;
           if (p.relu) {
 #pragma unroll
-            for (int j = 0; j < 32; ++j) bad |= !(v[j] <= 3.402823466e38f);
+            for (int j = 0; j < CH; ++j) bad |= !(v[j] <= 3.402823466e38f);
           } else {
 #pragma unroll
-            for (int j = 0; j < 32; ++j) bad |= !(v[j] >= 0.0f && v[j] <= 3.402823466e38f);
+            for (int j = 0; j < CH; ++j) bad |= !(v[j] >= 0.0f && v[j] <= 3.402823466e38f);
           }
           if (bad) tk_raise(p.err, (unsigned long long)qrow, TK_ERR_NONFINITE);
-          uint32_t w[8];
+          uint32_t w[CH / 4];
 #pragma unroll
           for (int o = 0; o < 2; ++o) {
             if (o >= p.n_q) break;
             if (o == 0 || !p.q_same) {
               const float t0 = p.t0[o], t1 = p.t1[o];
 #pragma unroll
-              for (int j = 0; j < 8; ++j) {
+              for (int j = 0; j < CH / 4; ++j) {
                 uint32_t b = 0;
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
@@ -478,11 +488,11 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
             const long long off = p.q_phases[o] == 4 ? ((long long)(chq * 4 + ph4) * p.q_pos[o] + P4) * Rq + cq
                                                      : ((long long)chq * p.q_pos[o] + P1) * Rq + cq;
             uint4* dst = reinterpret_cast<uint4*>(p.q[o] + off);
-            dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
-            dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+#pragma unroll
+            for (int j = 0; j < CH / 16; ++j) dst[j] = make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
           }
         }
-            }
+      }
       sm100::tc_fence_before();
       sm100::mbar_arrive(&a_empty[acc]);
     }
@@ -1041,7 +1051,7 @@ cudaError_t launch_conv(const Conv& cv, const float* x, cudaStream_t s) {
   }
   ConvK k = cv.k;
   if (cv.skip_f == -2) k.skip = x;  // identity shortcut = the forward's input
-  k_conv_tc<BN, R, KT, MT><<<cv.grid, kConvThreads, cv.smem, s>>>(cv.in_map, cv.w_map, k);
+  k_conv_tc<BN, R, KT, MT><<<cv.grid, conv_threads(BN, MT), cv.smem, s>>>(cv.in_map, cv.w_map, k);
   return cudaGetLastError();
 }
 

@@ -245,7 +245,11 @@ class ResNetWorkload:
                        "parallelism": f"batch-sharded dp{world}, logits gathered to rank 0",
                        "fused_pipeline": self.net.body.fused,
                        "body_gmac_per_img": round(self.macs_per_img / 1e9, 4),
-                       "l2": "flushed between steps (256 MB write)"}
+                       }
+        in_mb = batch * 64 * 56 * 56 * 4 / 2**20
+        self.needs_flush = in_mb <= 126
+        self.config["l2"] = ("flushed between steps (256 MB write)" if self.needs_flush else
+                             f"not flushed: the step's input ({in_mb:.0f} MB f32) exceeds the 126 MB L2")
 
     def step(self):
         return self.net.body.forward(self.x, pooled=self.pooled, check_errors=False)
