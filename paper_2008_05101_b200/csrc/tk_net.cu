@@ -45,7 +45,9 @@ namespace {
 // epilogue walks the accumulator row 16 columns at a time (<= 128 registers).
 // (a group waits on accumulator-buffer parity, so groups <= buffers: with
 // at most one pass of lead no waiter can match a stale phase)
-__host__ __device__ constexpr int conv_groups(int BN, int MT) { return MT == 2 ? 2 : (BN <= 128 ? 3 : 2); }
+__host__ __device__ constexpr int conv_groups(int BN, int MT) {
+  return MT == 2 ? 2 : (BN == 64 ? 4 : (BN <= 128 ? 3 : 2));
+}
 __host__ __device__ constexpr int conv_threads(int BN, int MT) { return 64 + 128 * conv_groups(BN, MT); }
 constexpr int CH = 16;  // accumulator columns per epilogue step
 
@@ -119,7 +121,7 @@ __device__ __forceinline__ unsigned long long gtime() {
 // per-item pipeline overhead); each accumulator buffer holds MT x BN columns
 template <int BN, int MT>
 struct Acc {
-  static constexpr int kN = BN * MT <= 128 ? 4 : 2;  // accumulator buffers
+  static constexpr int kN = BN * MT <= 128 ? 4 : (BN * MT <= 256 ? 2 : 1);  // accumulator buffers
   static constexpr uint32_t kCols = kN * BN * MT;    // TMEM columns (power of 2)
 };
 
@@ -163,6 +165,7 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
   if (stamp && threadIdx.x == 0) g_stamps[blockIdx.x * 8 + 0] = gtime();
 
   if (threadIdx.x == 0) {
+    sm100::pdl_launch_dependents();
     sm100::tma_prefetch(&in_map);
     sm100::tma_prefetch(&w_map);
     for (int s = 0; s < p.hs; ++s) {
@@ -206,6 +209,9 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
       for (int b = 0; b < p.chunks * p.n_taps; ++b)
         sm100::tma_load_2d(wreg + (size_t)b * p.WB, &w_map, w_res, 0, b * BN);
     }
+    // weights are constant: their loads overlap the previous layer's tail;
+    // activations only after that layer has completed (PDL)
+    sm100::pdl_wait();
     int hs_i = 0, h_round = 0, ws_i = 0, w_round = 0;
     int mt = blockIdx.x / p.n_tiles, nt = blockIdx.x - mt * p.n_tiles;
     const int dmt = gridDim.x / p.n_tiles, dnt = gridDim.x - dmt * p.n_tiles;
@@ -320,7 +326,7 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
     // the TMEM-load and memory latencies); within a group warp w owns TMEM
     // lane quarter w % 4 and walks all BN columns.
     constexpr int G = conv_groups(BN, MT), kEpiThreads = 128 * G;
-    static_assert(G <= kAcc, "epilogue groups must not outnumber accumulator buffers");
+    static_assert(MT == 2 || G <= kAcc, "epilogue groups must not outnumber accumulator buffers");
     const int et = threadIdx.x - 64;
     const int qtr = warp & 3;
     const int grp = (warp - 2) >> 2;
@@ -330,6 +336,7 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
       eparam[i] = p.ithr ? (uint32_t)__ldg(p.ithr + i)
                          : __float_as_uint(__ldg((i < p.N ? p.gain : p.bias - p.N) + i));
     epi_bar<kEpiThreads>();
+    sm100::pdl_wait();  // skip inputs / outputs of the neighbouring layers
     const uint32_t* ep = eparam;
     int it = 0;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
@@ -771,6 +778,7 @@ int prepare_conv_weights(Conv& cv, int R) {
   cv.R = R;
   cv.chunks = chunks;
   cv.BN = d.out_c >= 256 ? 256 : d.out_c;  // 64, 128, 256
+  if (getenv("TK_CONV_BNMAX")) cv.BN = std::min(cv.BN, std::max(64, atoi(getenv("TK_CONV_BNMAX"))));
   cv.n_tiles = d.out_c / cv.BN;
   const size_t blk = (size_t)cv.BN * R;
   std::vector<int8_t> w((size_t)cv.n_tiles * chunks * taps * blk, 0);
@@ -939,6 +947,7 @@ int setup_fused(tk_net* net) {
       // convs and wider layers run faster with the two epilogue groups on
       // alternate items)
       cv.MT = (cv.BN == 64 && cv.skip_f == -1 && cv.out_f < 0 && k.m_tiles > 1) ? 2 : 1;
+      if (getenv("TK_CONV_MT2WIDE") && cv.BN == 256 && k.m_tiles > 1) cv.MT = 2;  // experiment
       if (getenv("TK_CONV_MT")) cv.MT = std::min(cv.MT, std::max(1, atoi(getenv("TK_CONV_MT"))));
       k.m_items = (k.m_tiles + cv.MT - 1) / cv.MT;
       {
@@ -1051,13 +1060,27 @@ cudaError_t launch_conv(const Conv& cv, const float* x, cudaStream_t s) {
   }
   ConvK k = cv.k;
   if (cv.skip_f == -2) k.skip = x;  // identity shortcut = the forward's input
-  k_conv_tc<BN, R, KT, MT><<<cv.grid, conv_threads(BN, MT), cv.smem, s>>>(cv.in_map, cv.w_map, k);
-  return cudaGetLastError();
+  // programmatic dependent launch (env TK_PDL=1): the prologue (TMEM,
+  // barriers, resident weights) may overlap the previous kernel's tail.  Off
+  // by default: with one persistent CTA per SM no SM frees early enough for
+  // it to pay off (measured: tools/bench_pdl.sh)
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cv.grid);
+  cfg.blockDim = dim3(conv_threads(BN, MT));
+  cfg.dynamicSmemBytes = cv.smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  static const int pdl = getenv("TK_PDL") ? atoi(getenv("TK_PDL")) : 0;
+  at[0].val.programmaticStreamSerializationAllowed = pdl;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_conv_tc<BN, R, KT, MT>, cv.in_map, cv.w_map, k);
 }
 
 template <int BN, int R, int KT>
 cudaError_t launch_conv_mt(const Conv& cv, const float* x, cudaStream_t s) {
-  if constexpr (BN == 64) {
+  if constexpr (BN == 64 || BN == 256) {
     if (cv.MT == 2) return launch_conv<BN, R, KT, 2>(cv, x, s);
   }
   return launch_conv<BN, R, KT, 1>(cv, x, s);
