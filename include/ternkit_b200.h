@@ -207,6 +207,16 @@ int tk_net_is_fused(const tk_net* net);
  * [batch][C][H][W] f32; pooled (nullable): its spatial mean [batch][C]. */
 int tk_net_forward(tk_context* ctx, tk_net* net, const float* x, float* out,
                    float* pooled, void* stream);
+/* Network stem helper (float, outside the ternary path): the fused
+ * y = maxpool3x3/2(max(fmaf(gain[c], x, bias[c]), 0)) (pad 1, -inf padding)
+ * over x [n][c][h][w] f32 -> out [n][c][(h+1)/2][(w+1)/2], one pass. */
+int tk_affine_relu_maxpool(tk_context* ctx, const float* x, int n, int c, int h, int w,
+                           const float* gain, const float* bias, float* out, void* stream);
+/* Network stem helper: 7x7 / stride 2 / pad 3 convolution, 3 -> 64 channels,
+ * fp32 FMA in (ci, ky, kx) order: images [n][3][h][w] (w <= 224), weights
+ * [64][3][7][7] -> out [n][64][(h-1)/2+1][(w-1)/2+1] (no bias). */
+int tk_stem_conv7x7s2(tk_context* ctx, const float* images, int n, int h, int w, const float* weights,
+                      float* out, void* stream);
 /* number of kernel launches one tk_net_forward issues */
 int tk_net_launches(const tk_net* net, int with_out, int with_pooled);
 /* diagnostics: per-conv device time of the last forward after

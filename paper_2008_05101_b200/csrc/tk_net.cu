@@ -46,7 +46,7 @@ namespace {
 // (a group waits on accumulator-buffer parity, so groups <= buffers: with
 // at most one pass of lead no waiter can match a stale phase)
 __host__ __device__ constexpr int conv_groups(int BN, int MT) {
-  return MT == 2 ? 2 : (BN == 64 ? 4 : (BN <= 128 ? 3 : 2));
+  return MT == 2 ? 4 : (BN == 64 ? 4 : (BN <= 128 ? 3 : 2));
 }
 __host__ __device__ constexpr int conv_threads(int BN, int MT) { return 64 + 128 * conv_groups(BN, MT); }
 constexpr int CH = 16;  // accumulator columns per epilogue step
@@ -263,6 +263,7 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
     // descriptor templates: only the start-address field (bits 0-13, in
     // 16-byte units) changes per MMA
     const uint64_t tmpl = desc_sw(0, R);
+    const uint32_t dhi = (uint32_t)(tmpl >> 32);  // SBO, version, swizzle mode
     const uint32_t halo0 = sm100::smem_u32(halo), wreg0 = sm100::smem_u32(wreg);
     uint32_t toff[KT];
 #pragma unroll
@@ -282,27 +283,28 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
         if (stamp && lane == 0 && blockIdx.x == 0 && h_round * p.hs + hs_i < 32)
           g_trace[2 * 32 + h_round * p.hs + hs_i] = clock64();
         sm100::tc_fence_after();
-        const uint32_t hbase = halo0 + hs_i * halo_stage;
-        const uint32_t wres = wreg0 + (uint32_t)(ch * KT) * p.WB;
+        // descriptor low halves: start address >> 4 in bits 0-13 (smem
+        // addresses < 2^18, so per-MMA offsets are plain adds) | LBO = 1
+        const uint32_t a0 = ((halo0 + hs_i * halo_stage) >> 4) | (1u << 16);
+        const uint32_t wres = ((wreg0 + (uint32_t)(ch * KT) * p.WB) >> 4) | (1u << 16);
 #pragma unroll
         for (int t = 0; t < KT; ++t) {
-          uint32_t wb;
+          uint32_t b0;
           if (p.resident) {
-            wb = wres + (uint32_t)t * p.WB;
+            b0 = wres + (uint32_t)t * (p.WB >> 4);
           } else {
             sm100::mbar_wait(&w_full[ws_i], w_round & 1);
             sm100::tc_fence_after();
-            wb = wreg0 + (uint32_t)ws_i * p.WB;
+            b0 = (((wreg0 + (uint32_t)ws_i * p.WB)) >> 4) | (1u << 16);
           }
-          const uint32_t ab = hbase + toff[t];
+          const uint32_t at = a0 + (toff[t] >> 4);
           if (do_mma) {
 #pragma unroll
             for (int k = 0; k < kSteps; ++k)
 #pragma unroll
               for (int u = 0; u < MT; ++u)
-                sm100::mma_i8_elect(d + u * BN, tmpl | (uint64_t)(((ab + u * 128 * R + k * 32) & 0x3FFFFu) >> 4),
-                                    tmpl | (uint64_t)(((wb + k * 32) & 0x3FFFFu) >> 4), idesc,
-                                    (ci | t | k) != 0);
+                sm100::mma_i8_elect_lohi(d + u * BN, at + (uint32_t)((u * 128 * R + k * 32) >> 4), dhi,
+                                         b0 + (uint32_t)(k * 2), dhi, idesc, (ci | t | k) != 0);
           }
           if (!p.resident) {
             sm100::mma_commit_elect(&w_empty[ws_i]);
@@ -326,7 +328,7 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
     // the TMEM-load and memory latencies); within a group warp w owns TMEM
     // lane quarter w % 4 and walks all BN columns.
     constexpr int G = conv_groups(BN, MT), kEpiThreads = 128 * G;
-    static_assert(MT == 2 || G <= kAcc, "epilogue groups must not outnumber accumulator buffers");
+    static_assert(G / MT <= kAcc, "epilogue groups must not outnumber accumulator buffers");
     const int et = threadIdx.x - 64;
     const int qtr = warp & 3;
     const int grp = (warp - 2) >> 2;
@@ -340,11 +342,12 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
     const uint32_t* ep = eparam;
     int it = 0;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
-      // MT == 1: the groups take turns; MT == 2: group g takes M tile g of every item
-      if (MT == 1 && it % G != grp) continue;
+      // MT == 1: the groups take turns on items; MT == 2: group g takes M tile
+      // g % 2 of every (G/2)-th item
+      if (it % (G / MT) != grp / MT) continue;
       const int mi = item / p.n_tiles, nt = item - mi * p.n_tiles;
-      const int mt = mi * MT + (MT == 1 ? 0 : grp);
-      const uint32_t tcol = (uint32_t)(it % kAcc) * (BN * MT) + (MT == 1 ? 0 : grp * BN);
+      const int mt = mi * MT + (MT == 1 ? 0 : grp % 2);
+      const uint32_t tcol = (uint32_t)(it % kAcc) * (BN * MT) + (MT == 1 ? 0 : (grp % 2) * BN);
       const int acc = it % kAcc;
       if (p.dbg & 8) {  // profiling: bare accumulator hand-off
         if (!(p.dbg & 64) || lane == 0) sm100::mbar_wait(&a_full[acc], (it / kAcc) & 1);
@@ -378,7 +381,10 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
 #pragma unroll
         for (int j = 0; j < CH; ++j, off += ostride) sk[j] = __ldg(skp + off);
       }
-      sm100::mbar_wait(&a_full[acc], (it / kAcc) & 1);
+      if (p.dbg & 1024)
+        sm100::mbar_wait(&a_full[acc], (it / kAcc) & 1);
+      else
+        sm100::mbar_wait_sleep(&a_full[acc], (it / kAcc) & 1, 2000);
       sm100::tc_fence_after();
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += CH) {
@@ -419,6 +425,7 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
           }
           continue;
         }
+        if constexpr (MT == 2) continue;  // MT == 2 kernels: integer epilogue only (host-checked)
         const float4* eg = reinterpret_cast<const float4*>(ep + n0);
         const int n4 = p.N / 4;
         float v[CH];
@@ -586,6 +593,112 @@ __global__ void k_residual_relu(float* __restrict__ z, const float* __restrict__
 }
 
 // spatial mean -> [N][C] (head input; left-to-right float sum)
+// ---------------------------------------------------------------------------
+// stem convolution (float, outside the ternary path): 7x7 / stride 2 / pad 3,
+// 3 -> 64 channels, fp32 FMA accumulation in the fixed order (ci, ky, kx).
+// CTA = one image, kStemRows output rows x the full width; 256 threads =
+// 4 channel groups (16 channels) x 64 pixel groups (7 consecutive columns of
+// one row), 112 accumulators per thread.  Input band and weights in SMEM;
+// per tap 4 x LDS.128 (weights, broadcast) + 7 LDS (inputs) feed 112 FFMA.
+constexpr int kStemRows = 4, kStemCols = 112, kStemPx = 7;
+constexpr int kStemInRows = 2 * kStemRows + 5, kStemInCols = 2 * kStemCols + 6;
+// the input band is stored as even / odd column planes (stride-2 taps read
+// consecutive words); plane pitch 120 = 8 mod 16 puts the two image rows a
+// warp reads 16 banks apart: conflict-free shared loads
+constexpr int kStemHalf = kStemInCols / 2, kStemPitch = 120;
+constexpr int kStemSmem = (147 * 64 + 3 * kStemInRows * 2 * kStemPitch) * 4;
+
+__global__ void __launch_bounds__(256, 1)
+k_stem_conv(const float* __restrict__ img, const float* __restrict__ wgt, int H, int W, int Ho, int Wo,
+            float* __restrict__ out) {
+  extern __shared__ __align__(16) float s_stem[];
+  float* s_w = s_stem;                 // [tap][cout]
+  float* s_in = s_stem + 147 * 64;     // [ci][row][parity][kStemPitch]
+  const int n = blockIdx.y, oy0 = blockIdx.x * kStemRows;
+  for (int i = threadIdx.x; i < 147 * 64; i += 256) {
+    const int co = i / 147, tap = i - co * 147;  // weights [cout][ci][ky][kx]
+    s_w[tap * 64 + co] = __ldg(wgt + i);
+  }
+  for (int i = threadIdx.x; i < 3 * kStemInRows * kStemInCols; i += 256) {
+    const int ci = i / (kStemInRows * kStemInCols);
+    const int r = (i / kStemInCols) % kStemInRows, c = i % kStemInCols;
+    const int y = 2 * oy0 - 3 + r, x = c - 3;
+    s_in[((ci * kStemInRows + r) * 2 + (c & 1)) * kStemPitch + (c >> 1)] =
+        (y >= 0 && y < H && x >= 0 && x < W) ? __ldg(img + ((size_t)(n * 3 + ci) * H + y) * W + x) : 0.0f;
+  }
+  __syncthreads();
+  const int cg = threadIdx.x >> 6;      // channel group of 16 (warp-uniform)
+  const int pg = threadIdx.x & 63;
+  const int row = pg >> 4, c0 = pg & 15;  // output columns c0, c0+16, ..., c0+96
+  float acc[16][kStemPx];
+#pragma unroll
+  for (int c = 0; c < 16; ++c)
+#pragma unroll
+    for (int j = 0; j < kStemPx; ++j) acc[c][j] = 0.0f;
+  for (int ci = 0; ci < 3; ++ci)
+#pragma unroll 1
+    for (int ky = 0; ky < 7; ++ky) {
+      const float* in_row = s_in + (ci * kStemInRows + 2 * row + ky) * 2 * kStemPitch;
+#pragma unroll
+      for (int kx = 0; kx < 7; ++kx) {
+        const float4* w4 = reinterpret_cast<const float4*>(s_w + ((ci * 7 + ky) * 7 + kx) * 64 + cg * 16);
+        float wv[16];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float4 t = w4[q];
+          wv[4 * q] = t.x; wv[4 * q + 1] = t.y; wv[4 * q + 2] = t.z; wv[4 * q + 3] = t.w;
+        }
+        // input column 2*oc + kx (band coordinates) = plane kx&1, word oc + kx/2
+        const float* pl = in_row + (kx & 1) * kStemPitch + (kx >> 1) + c0;
+        float xv[kStemPx];
+#pragma unroll
+        for (int j = 0; j < kStemPx; ++j) xv[j] = pl[16 * j];
+#pragma unroll
+        for (int c = 0; c < 16; ++c)
+#pragma unroll
+          for (int j = 0; j < kStemPx; ++j) acc[c][j] = __fmaf_rn(wv[c], xv[j], acc[c][j]);
+      }
+    }
+  const int oy = oy0 + row;
+  if (oy >= Ho) return;
+#pragma unroll
+  for (int c = 0; c < 16; ++c) {
+    float* o = out + ((size_t)(n * 64 + cg * 16 + c) * Ho + oy) * Wo;
+#pragma unroll
+    for (int j = 0; j < kStemPx; ++j)
+      if (c0 + 16 * j < Wo) o[c0 + 16 * j] = acc[c][j];
+  }
+}
+
+// stem: out = maxpool3x3/2 pad 1 (relu(fmaf(g, x, b))); thread per output
+__global__ void k_affine_relu_maxpool(const float* __restrict__ x, int C, int H, int W, int Ho, int Wo,
+                                      const float* __restrict__ gain, const float* __restrict__ bias,
+                                      long long total, float* __restrict__ out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int ox = (int)(i % Wo);
+    const long long r = i / Wo;
+    const int oy = (int)(r % Ho);
+    const long long nc = r / Ho;
+    const int c = (int)(nc % C);
+    const float g = __ldg(gain + c), b = __ldg(bias + c);
+    const float* src = x + nc * H * W;
+    float m = 0.0f;  // relu output >= 0, so 0 is the identity of the max
+    for (int dy = -1; dy <= 1; ++dy) {
+      const int y = 2 * oy + dy;
+      if (y < 0 || y >= H) continue;
+#pragma unroll
+      for (int dx = -1; dx <= 1; ++dx) {
+        const int xx = 2 * ox + dx;
+        if (xx < 0 || xx >= W) continue;
+        const float v = __fmaf_rn(g, __ldg(src + (long long)y * W + xx), b);
+        m = fmaxf(m, v);
+      }
+    }
+    out[i] = m;
+  }
+}
+
 __global__ void k_pool_nchw(const float* __restrict__ x, int NC, int HW, float* __restrict__ out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= NC) return;
@@ -946,8 +1059,14 @@ int setup_fused(tk_net* net) {
       // (measured: pays off for the 64-channel inner convs; the f32-epilogue
       // convs and wider layers run faster with the two epilogue groups on
       // alternate items)
-      cv.MT = (cv.BN == 64 && cv.skip_f == -1 && cv.out_f < 0 && k.m_tiles > 1) ? 2 : 1;
-      if (getenv("TK_CONV_MT2WIDE") && cv.BN == 256 && k.m_tiles > 1) cv.MT = 2;  // experiment
+      // integer-threshold (inner) convs: ReLU + quantize only, no floats out
+      bool inner = cv.relu && cv.skip_f == -1 && cv.out_f < 0 && cv.q_idx[0] >= 0;
+      if (inner) {
+        tk_qparams q0;
+        const S8T& q = net->s8[cv.q_idx[0]];
+        inner = tk_make_qparams(q.ta1, q.ta2, TK_MODE_ACTIVATION_NONNEG, &q0) == TK_OK && q0.t0 >= 0.0f;
+      }
+      cv.MT = (cv.BN == 64 && inner && k.m_tiles > 1) ? 2 : 1;  // MT = 2 kernels carry the integer epilogue only
       if (getenv("TK_CONV_MT")) cv.MT = std::min(cv.MT, std::max(1, atoi(getenv("TK_CONV_MT"))));
       k.m_items = (k.m_tiles + cv.MT - 1) / cv.MT;
       {
@@ -1020,6 +1139,7 @@ int setup_fused(tk_net* net) {
         cudaMemcpy(cv.d_ithr, thr.data(), thr.size() * 4, cudaMemcpyHostToDevice);
         k.ithr = cv.d_ithr;
       }
+      if (cv.MT == 2 && !k.ithr) return TK_ERR_UNSUPPORTED;  // (inner predicate above mirrors this)
       k.err = net->ctx->d_err;
       k.dbg = getenv("TK_CONV_DBG") ? atoi(getenv("TK_CONV_DBG")) : 0;
       // profiling: TK_CONV_DBG_ONLY=<launch order index> limits the knob to one conv
@@ -1080,7 +1200,7 @@ cudaError_t launch_conv(const Conv& cv, const float* x, cudaStream_t s) {
 
 template <int BN, int R, int KT>
 cudaError_t launch_conv_mt(const Conv& cv, const float* x, cudaStream_t s) {
-  if constexpr (BN == 64 || BN == 256) {
+  if constexpr (BN == 64) {
     if (cv.MT == 2) return launch_conv<BN, R, KT, 2>(cv, x, s);
   }
   return launch_conv<BN, R, KT, 1>(cv, x, s);
@@ -1182,6 +1302,34 @@ int tk_net_create(tk_context* ctx, const tk_block_desc* blocks, int n_blocks, in
   cudaDeviceSynchronize();
   *out = net;
   return TK_OK;
+}
+
+int tk_affine_relu_maxpool(tk_context* ctx, const float* x, int n, int c, int h, int w, const float* gain,
+                           const float* bias, float* out, void* stream) {
+  if (!ctx || !x || !gain || !bias || !out || n < 0 || c <= 0 || h <= 0 || w <= 0) return TK_ERR_INVALID;
+  const int ho = (h + 1) / 2, wo = (w + 1) / 2;
+  const long long total = (long long)n * c * ho * wo;
+  if (total == 0) return TK_OK;
+  const unsigned grid = (unsigned)std::min<long long>((total + 255) / 256, 148ll * 64);
+  k_affine_relu_maxpool<<<grid, 256, 0, (cudaStream_t)stream>>>(x, c, h, w, ho, wo, gain, bias, total, out);
+  return cudaGetLastError() == cudaSuccess ? TK_OK : TK_ERR_CUDA;
+}
+
+int tk_stem_conv7x7s2(tk_context* ctx, const float* images, int n, int h, int w, const float* weights,
+                      float* out, void* stream) {
+  if (!ctx || !images || !weights || !out || n < 0 || h <= 0 || w <= 0) return TK_ERR_INVALID;
+  const int ho = (h + 6 - 7) / 2 + 1, wo = (w + 6 - 7) / 2 + 1;
+  if (wo > kStemCols || (w + 6) > kStemInCols) return TK_ERR_UNSUPPORTED;  // one CTA spans the width
+  if (n == 0) return TK_OK;
+  dim3 grid((ho + kStemRows - 1) / kStemRows, n);
+  const int smem = kStemSmem;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_stem_conv, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  k_stem_conv<<<grid, 256, smem, (cudaStream_t)stream>>>(images, weights, h, w, ho, wo, out);
+  return cudaGetLastError() == cudaSuccess ? TK_OK : TK_ERR_CUDA;
 }
 
 int tk_net_destroy(tk_net* net) {

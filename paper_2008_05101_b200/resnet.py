@@ -191,15 +191,69 @@ class TernaryResNet:
         self.head_b = torch.zeros(classes).cuda()
 
     def stem(self, images: torch.Tensor) -> torch.Tensor:
-        with torch.backends.cudnn.flags(enabled=True, allow_tf32=False):
-            y = torch.nn.functional.conv2d(images, self.stem_w, stride=2, padding=3)
-        y = torch.relu(y * self.stem_gain.view(1, -1, 1, 1) + self.stem_bias.view(1, -1, 1, 1))
-        return torch.nn.functional.max_pool2d(y, 3, 2, 1).contiguous()
+        """fp32 7x7/2 conv (tk_stem_conv7x7s2: SIMT FMA, no tensor-core
+        rounding), then one fused pass of folded BN (fmaf), ReLU and 3x3/2
+        max-pool (tk_affine_relu_maxpool)."""
+        images = images.contiguous()
+        n = images.shape[0]
+        y = torch.empty((n, 64, 112, 112), dtype=torch.float32, device="cuda")
+        if os.environ.get("TK_STEM") == "cudnn":
+            with torch.backends.cudnn.flags(enabled=True, allow_tf32=False):
+                y = torch.nn.functional.conv2d(images, self.stem_w, stride=2, padding=3)
+        else:
+            check(T.lib().tk_stem_conv7x7s2(tk.context(), images.data_ptr(), n, images.shape[2], images.shape[3],
+                                            self.stem_w.data_ptr(), y.data_ptr(), tk._stream()),
+                  "tk_stem_conv7x7s2")
+        n, c, h, w = y.shape
+        out = torch.empty((n, c, (h + 1) // 2, (w + 1) // 2), dtype=torch.float32, device="cuda")
+        check(T.lib().tk_affine_relu_maxpool(tk.context(), y.data_ptr(), n, c, h, w, self.stem_gain.data_ptr(),
+                                             self.stem_bias.data_ptr(), out.data_ptr(), tk._stream()),
+              "tk_affine_relu_maxpool")
+        return out
+
+    def head(self, pooled: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        return torch.addmm(self.head_b, pooled, self.head_w.t(), beta=1.0, alpha=1.0, out=out)
 
     def forward(self, images: torch.Tensor, check_errors: bool = False) -> torch.Tensor:
         x = self.stem(images)
         pooled = self.body.forward(x, check_errors=check_errors)
-        return torch.addmm(self.head_b, pooled, self.head_w.t(), beta=1.0, alpha=1.0)
+        return self.head(pooled)
+
+
+class PipelinedResNet:
+    """End-to-end inference from host images with the host->device copy of
+    image chunk i+1 (copy stream) overlapping stem + body + head of chunk i
+    (compute stream).  Shares the stem/head parameters and block spec of
+    `net`; the body runs on `chunk`-image slices (its own TernaryBody)."""
+
+    def __init__(self, net: TernaryResNet, batch: int, chunks: int = 4):
+        assert batch % chunks == 0
+        self.net, self.batch, self.chunks, self.cb = net, batch, chunks, batch // chunks
+        self.body = TernaryBody(net.blocks, self.cb, 64, 56, 56)
+        self.copy_stream = torch.cuda.Stream()
+        self.img = [torch.empty((self.cb, 3, 224, 224), device="cuda") for _ in range(chunks)]
+        self.ev_copied = [torch.cuda.Event() for _ in range(chunks)]
+        self.ev_consumed = [torch.cuda.Event() for _ in range(chunks)]
+        self.pooled = torch.empty((batch, self.body.out_shape[0]), device="cuda")
+        self.logits = torch.empty((batch, net.head_w.shape[0]), device="cuda")
+        self._first = True
+
+    def forward(self, images_host: torch.Tensor) -> torch.Tensor:
+        cs = torch.cuda.current_stream()
+        self.copy_stream.wait_stream(cs)  # previous users of the outputs are ordered
+        for i in range(self.chunks):
+            sl = slice(i * self.cb, (i + 1) * self.cb)
+            with torch.cuda.stream(self.copy_stream):
+                if not self._first:  # the previous step's stem has read this buffer
+                    self.copy_stream.wait_event(self.ev_consumed[i])
+                self.img[i].copy_(images_host[sl], non_blocking=True)
+                self.ev_copied[i].record(self.copy_stream)
+            cs.wait_event(self.ev_copied[i])
+            x = self.net.stem(self.img[i])
+            self.ev_consumed[i].record(cs)
+            self.body.forward(x, pooled=self.pooled[sl], check_errors=False)
+        self._first = False
+        return self.net.head(self.pooled, out=self.logits)
 
 
 # ---------------------------------------------------------------------------
@@ -232,8 +286,11 @@ class ResNetWorkload:
         self.x = self.net.stem(self.images_dev)  # body input, resident
         self.pooled = torch.empty((batch, self.net.body.out_shape[0]), device="cuda")
         self.logits_host = torch.empty((global_batch if rank == 0 else 0, 1000)).pin_memory()
-        self.img_dev2 = torch.empty_like(self.images_dev)
-        self.sharded = ShardedForward(self.net.forward, global_batch, 1000, rank, world)
+        # e2e: chunked so the image upload overlaps the compute of earlier chunks
+        chunks = int(os.environ.get("TK_E2E_CHUNKS", 4 if batch % 4 == 0 and batch >= 64 else 1))
+        self.pipe = PipelinedResNet(self.net, batch, chunks)
+        self.sharded = ShardedForward(lambda _x: self.pipe.forward(self.images_host), global_batch, 1000, rank,
+                                      world)
         self.macs_per_img = body_macs(self.net.blocks)
         self.units_per_step = float(global_batch)  # whole job, all ranks
         self.unit = "img/s"
@@ -257,8 +314,7 @@ class ResNetWorkload:
     def step_e2e(self):
         """Host images -> stem -> ternary body -> head on this rank's shard,
         logits gathered to rank 0 (the only collective) and read back."""
-        self.img_dev2.copy_(self.images_host, non_blocking=True)
-        logits = self.sharded(self.img_dev2)
+        logits = self.sharded(None)  # PipelinedResNet uploads the images chunk by chunk
         if logits is not None:
             self.logits_host.copy_(logits, non_blocking=True)
         return logits

@@ -113,3 +113,38 @@ def test_net_errors(tk):
                        conv_spec(np.random.default_rng(0), 64, 32, 3, 1, 1)])]  # identity shape mismatch
     with pytest.raises(tk.InvalidArgument):
         TernaryBody(bad, 1, 64, 8, 8)
+
+
+def test_pipelined_e2e_matches_serial_chunks(tk):
+    """PipelinedResNet (chunked H2D overlapping compute) == the same chunks run
+    serially through stem -> body -> head; stem pooling == torch reference."""
+    from paper_2008_05101_b200.resnet import PipelinedResNet, TernaryBody, TernaryResNet
+    net = TernaryResNet(18, 16, seed=3)
+    pipe = PipelinedResNet(net, 16, chunks=4)
+    g = torch.Generator().manual_seed(5)
+    imgs = torch.rand(16, 3, 224, 224, generator=g).pin_memory()
+    got = pipe.forward(imgs).clone()
+    body4 = TernaryBody(net.blocks, 4, 64, 56, 56)
+    pooled = torch.cat([body4.forward(net.stem(imgs[4 * i:4 * i + 4].cuda())) for i in range(4)])
+    torch.cuda.synchronize()
+    assert torch.equal(pipe.pooled, pooled)  # stem + ternary body, chunk by chunk: bit-exact
+    assert torch.equal(got, net.head(pooled))  # (one head GEMM over the whole batch, as the pipeline does)
+    # fused affine + ReLU + max-pool vs torch (fmaf vs mul+add: within 1 ulp-ish)
+    y = torch.nn.functional.conv2d(imgs[:2].cuda(), net.stem_w, stride=2, padding=3)
+    ref = torch.nn.functional.max_pool2d(torch.relu(torch.addcmul(net.stem_bias.view(1, -1, 1, 1), y,
+                                                                  net.stem_gain.view(1, -1, 1, 1))), 3, 2, 1)
+    assert torch.allclose(net.stem(imgs[:2].cuda()), ref, rtol=1e-6, atol=1e-6)
+
+
+def test_stem_conv_matches_fp32_reference(tk):
+    """tk_stem_conv7x7s2 == torch fp32 conv2d (no TF32) within fp32 summation-order noise."""
+    from paper_2008_05101_b200.resnet import TernaryResNet
+    from paper_2008_05101_b200 import _lib as T
+    net = TernaryResNet(18, 2, seed=1)
+    x = torch.rand(3, 3, 224, 224, device="cuda")
+    y = torch.empty(3, 64, 112, 112, device="cuda")
+    T.check(T.lib().tk_stem_conv7x7s2(tk.context(), x.data_ptr(), 3, 224, 224, net.stem_w.data_ptr(),
+                                      y.data_ptr(), tk._stream()), "stem")
+    with torch.backends.cudnn.flags(enabled=True, allow_tf32=False):
+        ref = torch.nn.functional.conv2d(x.double(), net.stem_w.double(), stride=2, padding=3)
+    assert torch.allclose(y.double(), ref, rtol=1e-5, atol=1e-5)
