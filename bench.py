@@ -543,8 +543,17 @@ def run_ours(args) -> None:
     else:
         peak, psrc = peaks["hbm_gbs"], "MEASURED_PEAKS.json hbm_gbs"
     achieved = r["work"] / (r["avg_launch_ms"] / 1e3)
+    traffic = r.get("traffic")
+    tfile = os.path.join(ROOT, "profiles", "traffic_r01.json")
+    if traffic is None and os.path.exists(tfile):
+        tr = json.load(open(tfile)).get(args.workload)
+        if tr:
+            scale = (w.B / tr["batch"]) if tr.get("batch") else 1.0
+            traffic = {"bytes_per_launch": round(tr["bytes_per_launch"] * scale), "launches": tr["launches"],
+                       "source": tr["source"] + (f", scaled x{scale:g} from batch {tr['batch']}"
+                                                 if scale != 1.0 else "") + " (profiles/traffic_r01.json)"}
     roof = {"kernel": r["kernel"], "bound": r["bound"], "achieved": round(achieved, 3), "peak": round(peak, 2),
-            "unit": r["unit"], "frac": round(achieved / peak, 4), "traffic": r.get("traffic"),
+            "unit": r["unit"], "frac": round(achieved / peak, 4), "traffic": traffic,
             "peak_source": psrc, "avg_launch_ms": round(r["avg_launch_ms"], 5),
             "algorithmic": r.get("algorithmic")}
     for k in ("per_layer", "launches_timed"):

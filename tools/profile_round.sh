@@ -1,0 +1,27 @@
+#!/bin/bash
+# Round profiling: bench lines for every workload, the ncu launch list of the
+# default bench command, and DRAM traffic per launch of each workload's
+# dominant kernel (ncu, cold caches as ncu runs them).  Outputs: gpurun_out/prof/
+set -x
+mkdir -p gpurun_out/prof
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/prof/build.log 2>&1 || exit 1
+for w in resnet18 resnet50 fc dot conv; do
+  timeout 900 python bench.py --workload $w --steps 20 --warmup 5 > gpurun_out/prof/bench_$w.json 2> gpurun_out/prof/bench_$w.err
+done
+# launch list of the default bench command (kernel durations, serialised)
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/prof/launches_resnet18.csv \
+  python bench.py --steps 3 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
+# DRAM traffic of the dominant kernels
+M=dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum
+timeout 900 ncu --metrics $M --clock-control none --csv -k regex:k_conv_tc -c 19 --log-file gpurun_out/prof/traffic_resnet18.csv \
+  python tools/prof_net.py > /dev/null 2>&1
+DEPTH=50 B=128 timeout 900 ncu --metrics $M --clock-control none --csv -k regex:k_conv_tc -c 52 --log-file gpurun_out/prof/traffic_resnet50.csv \
+  python tools/prof_net.py > /dev/null 2>&1
+timeout 600 ncu --metrics $M --clock-control none --csv -k regex:k_gemm_tc -c 1 --log-file gpurun_out/prof/traffic_fc.csv \
+  python tools/prof_fc.py > /dev/null 2>&1
+timeout 600 ncu --metrics $M --clock-control none --csv -k regex:k_dot_batched -c 1 --log-file gpurun_out/prof/traffic_dot.csv \
+  python bench.py --workload dot --steps 3 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
+# one full-set capture of the top ResNet-18 conv (stage-1 conv with skip + f32 out)
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_conv_tc -s 1 -c 1 \
+  -o gpurun_out/prof/full_r18_conv1 python tools/prof_net.py > gpurun_out/prof/full.log 2>&1
+ls -la gpurun_out/prof
