@@ -46,10 +46,17 @@ namespace {
 // (a group waits on accumulator-buffer parity, so groups <= buffers: with
 // at most one pass of lead no waiter can match a stale phase)
 __host__ __device__ constexpr int conv_groups(int BN, int MT) {
-  return MT == 2 ? 4 : (BN == 64 ? 4 : (BN <= 128 ? 3 : 2));
+  return MT >= 2 ? 4 : (BN == 64 ? 4 : (BN <= 128 ? 3 : 2));
 }
 __host__ __device__ constexpr int conv_threads(int BN, int MT) { return 64 + 128 * conv_groups(BN, MT); }
-constexpr int CH = 16;  // accumulator columns per epilogue step
+// accumulator columns per epilogue step: 16 keeps 3-4 groups within 128 /
+// 96 registers; with 2 groups (168 registers) 32 columns double the f32
+// skip loads in flight per thread (the wide 1x1 f32-epilogue layers of
+// ResNet-50 are HBM-latency bound)
+// (measured: pays off on the 1x1 layers; the 3x3 ones spill)
+__host__ __device__ constexpr int conv_chunk(int BN, int MT, int KT) {
+  return conv_groups(BN, MT) == 2 && KT == 1 ? 32 : 16;
+}
 
 struct ConvK {
   int n_taps;
@@ -72,6 +79,7 @@ struct ConvK {
   const float* gain;
   const float* bias;
   const int* ithr;  // [n_q][3][N] (c0, c1, sign) integer-threshold mode, or null
+  int ithr16;       // ithr holds [n_q][N] (c0 & 0xffff) | c1 << 16 (all signs +1)
   float out_scale;
   int relu;
   int N;
@@ -145,7 +153,7 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
   // epilogue parameters of all N channels, staged once: int mode
   // [n_q][3][N] (c0, c1, sign), float mode [2][N] (gain, bias)
   uint32_t* eparam = reinterpret_cast<uint32_t*>(wreg + (size_t)wblocks * p.WB);
-  const int ewords = p.ithr ? p.n_q * 3 * p.N : 2 * p.N;
+  const int ewords = p.ithr ? (p.ithr16 ? p.n_q * p.N : p.n_q * 3 * p.N) : 2 * p.N;
   uint64_t* bars = reinterpret_cast<uint64_t*>(eparam + ((ewords + 1) & ~1));
   uint64_t* h_full = bars;
   uint64_t* h_empty = h_full + p.hs;
@@ -328,6 +336,7 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
     // the TMEM-load and memory latencies); within a group warp w owns TMEM
     // lane quarter w % 4 and walks all BN columns.
     constexpr int G = conv_groups(BN, MT), kEpiThreads = 128 * G;
+    constexpr int CH = conv_chunk(BN, MT, KT);
     static_assert(G / MT <= kAcc, "epilogue groups must not outnumber accumulator buffers");
     const int et = threadIdx.x - 64;
     const int qtr = warp & 3;
@@ -342,12 +351,12 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
     const uint32_t* ep = eparam;
     int it = 0;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
-      // MT == 1: the groups take turns on items; MT == 2: group g takes M tile
-      // g % 2 of every (G/2)-th item
+      // MT == 1: the groups take turns on items; MT > 1: group g takes M tile
+      // g % MT of every (G/MT)-th item
       if (it % (G / MT) != grp / MT) continue;
       const int mi = item / p.n_tiles, nt = item - mi * p.n_tiles;
-      const int mt = mi * MT + (MT == 1 ? 0 : grp % 2);
-      const uint32_t tcol = (uint32_t)(it % kAcc) * (BN * MT) + (MT == 1 ? 0 : (grp % 2) * BN);
+      const int mt = mi * MT + grp % MT;
+      const uint32_t tcol = (uint32_t)(it % kAcc) * (BN * MT) + (grp % MT) * BN;
       const int acc = it % kAcc;
       if (p.dbg & 8) {  // profiling: bare accumulator hand-off
         if (!(p.dbg & 64) || lane == 0) sm100::mbar_wait(&a_full[acc], (it / kAcc) & 1);
@@ -389,7 +398,10 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += CH) {
         uint32_t r[CH];
-        sm100::tmem_ld16(tmem + ((uint32_t)(qtr * 32) << 16) + tcol + c0, r);
+        if constexpr (CH == 32)
+          sm100::tmem_ld32(tmem + ((uint32_t)(qtr * 32) << 16) + tcol + c0, r);
+        else
+          sm100::tmem_ld16(tmem + ((uint32_t)(qtr * 32) << 16) + tcol + c0, r);
         sm100::tmem_ld_wait();
         if (!valid || (p.dbg & 4)) continue;
         const int n0 = nt * BN + c0;
@@ -398,22 +410,42 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
 #pragma unroll
           for (int o = 0; o < 2; ++o) {
             if (o >= p.n_q) break;
-            // (c0, c1, sign) of 4 channels per 16-byte LDS (broadcast: all
-            // lanes read the same channels)
-            const int4* e0 = reinterpret_cast<const int4*>(ep + o * 3 * p.N + n0);
-            const int n4 = p.N / 4;
             uint32_t w[CH / 4];
+            if (p.ithr16) {
+              // (c0, c1) s16 pairs of 4 channels per 16-byte LDS (broadcast):
+              // a third of the shared-memory wavefronts of the general form,
+              // which competes with the MMA operand reads
+              const uint4* e0 = reinterpret_cast<const uint4*>(ep + o * p.N + n0);
 #pragma unroll
-            for (int j = 0; j < CH / 4; ++j) {
-              const int4 lo = e0[j], hi = e0[n4 + j], sg = e0[2 * n4 + j];
-              const int xs[4] = {(int)r[4 * j] * sg.x, (int)r[4 * j + 1] * sg.y, (int)r[4 * j + 2] * sg.z,
-                                 (int)r[4 * j + 3] * sg.w};
-              const int l0[4] = {lo.x, lo.y, lo.z, lo.w}, l1[4] = {hi.x, hi.y, hi.z, hi.w};
-              uint32_t b = 0;
+              for (int j = 0; j < CH / 4; ++j) {
+                const uint4 cc = e0[j];
+                const uint32_t cw[4] = {cc.x, cc.y, cc.z, cc.w};
+                uint32_t b = 0;
 #pragma unroll
-              for (int i = 0; i < 4; ++i)
-                b |= ((uint32_t)(xs[i] > l0[i]) + (uint32_t)(xs[i] > l1[i])) << (8 * i);
-              w[j] = b;
+                for (int i = 0; i < 4; ++i) {
+                  const int x = (int)r[4 * j + i];
+                  b += ((x > (int)(int16_t)(cw[i] & 0xFFFFu)) ? (1u << (8 * i)) : 0u) +
+                       ((x > ((int)cw[i] >> 16)) ? (1u << (8 * i)) : 0u);
+                }
+                w[j] = b;
+              }
+            } else {
+              // (c0, c1, sign) of 4 channels per 16-byte LDS (broadcast: all
+              // lanes read the same channels)
+              const int4* e0 = reinterpret_cast<const int4*>(ep + o * 3 * p.N + n0);
+              const int n4 = p.N / 4;
+#pragma unroll
+              for (int j = 0; j < CH / 4; ++j) {
+                const int4 lo = e0[j], hi = e0[n4 + j], sg = e0[2 * n4 + j];
+                const int xs[4] = {(int)r[4 * j] * sg.x, (int)r[4 * j + 1] * sg.y, (int)r[4 * j + 2] * sg.z,
+                                   (int)r[4 * j + 3] * sg.w};
+                const int l0[4] = {lo.x, lo.y, lo.z, lo.w}, l1[4] = {hi.x, hi.y, hi.z, hi.w};
+                uint32_t b = 0;
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                  b |= ((uint32_t)(xs[i] > l0[i]) + (uint32_t)(xs[i] > l1[i])) << (8 * i);
+                w[j] = b;
+              }
             }
             const int Rq = p.q_R[o];
             const int chq = n0 / Rq, cq = n0 - chq * Rq;
@@ -425,7 +457,7 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
           }
           continue;
         }
-        if constexpr (MT == 2) continue;  // MT == 2 kernels: integer epilogue only (host-checked)
+        if constexpr (MT >= 2) continue;  // MT > 1 kernels: integer epilogue only (host-checked)
         const float4* eg = reinterpret_cast<const float4*>(ep + n0);
         const int n4 = p.N / 4;
         float v[CH];
@@ -1066,7 +1098,9 @@ int setup_fused(tk_net* net) {
         const S8T& q = net->s8[cv.q_idx[0]];
         inner = tk_make_qparams(q.ta1, q.ta2, TK_MODE_ACTIVATION_NONNEG, &q0) == TK_OK && q0.t0 >= 0.0f;
       }
-      cv.MT = (cv.BN == 64 && inner && k.m_tiles > 1) ? 2 : 1;  // MT = 2 kernels carry the integer epilogue only
+      // (MT > 1 kernels carry the integer epilogue only)
+      // (MT = 4 measured no faster than 2 on the ResNet-18 stage-1 convs)
+      cv.MT = (cv.BN == 64 && inner && k.m_tiles > 1) ? 2 : 1;
       if (getenv("TK_CONV_MT")) cv.MT = std::min(cv.MT, std::max(1, atoi(getenv("TK_CONV_MT"))));
       k.m_items = (k.m_tiles + cv.MT - 1) / cv.MT;
       {
@@ -1120,6 +1154,7 @@ int setup_fused(tk_net* net) {
       k.q_same = k.n_q == 2 && k.t0[0] == k.t0[1] && k.t1[0] == k.t1[1];
       // integer-threshold epilogue for inner convs (ReLU + quantize only)
       k.ithr = nullptr;
+      k.ithr16 = 0;
       if (cv.relu && cv.skip_f == -1 && cv.out_f < 0 && k.n_q > 0 && k.t0[0] >= 0.0f) {
         const int N = cv.d.out_c, kmax = 2 * cv.d.in_c * cv.d.k * cv.d.k;
         std::vector<int> thr((size_t)k.n_q * 3 * N);
@@ -1135,11 +1170,29 @@ int setup_fused(tk_net* net) {
             thr[((size_t)o * 3 + 1) * N + n] = c1;
             thr[((size_t)o * 3 + 2) * N + n] = s0;  // s0 == s1 (same direction)
           }
+        // compact form when every direction is +1 and the thresholds fit s16
+        bool pack16 = true;
+        for (int o = 0; o < k.n_q && pack16; ++o)
+          for (int n = 0; n < N && pack16; ++n) {
+            const int c0 = thr[((size_t)o * 3 + 0) * N + n], c1 = thr[((size_t)o * 3 + 1) * N + n];
+            pack16 = thr[((size_t)o * 3 + 2) * N + n] == 1 && c0 >= -32768 && c0 <= 32767 && c1 >= -32768 &&
+                     c1 <= 32767;
+          }
+        if (getenv("TK_CONV_NOPACK16")) pack16 = false;  // experiments
+        k.ithr16 = pack16 ? 1 : 0;
+        if (pack16) {
+          std::vector<int> p16((size_t)k.n_q * N);
+          for (int o = 0; o < k.n_q; ++o)
+            for (int n = 0; n < N; ++n)
+              p16[(size_t)o * N + n] = (int)(((uint32_t)thr[((size_t)o * 3 + 0) * N + n] & 0xFFFFu) |
+                                             ((uint32_t)thr[((size_t)o * 3 + 1) * N + n] << 16));
+          thr.swap(p16);
+        }
         if (cudaMalloc(&cv.d_ithr, thr.size() * 4) != cudaSuccess) return TK_ERR_CUDA;
         cudaMemcpy(cv.d_ithr, thr.data(), thr.size() * 4, cudaMemcpyHostToDevice);
         k.ithr = cv.d_ithr;
       }
-      if (cv.MT == 2 && !k.ithr) return TK_ERR_UNSUPPORTED;  // (inner predicate above mirrors this)
+      if (cv.MT > 1 && !k.ithr) return TK_ERR_UNSUPPORTED;  // (inner predicate above mirrors this)
       k.err = net->ctx->d_err;
       k.dbg = getenv("TK_CONV_DBG") ? atoi(getenv("TK_CONV_DBG")) : 0;
       // profiling: TK_CONV_DBG_ONLY=<launch order index> limits the knob to one conv
@@ -1201,6 +1254,7 @@ cudaError_t launch_conv(const Conv& cv, const float* x, cudaStream_t s) {
 template <int BN, int R, int KT>
 cudaError_t launch_conv_mt(const Conv& cv, const float* x, cudaStream_t s) {
   if constexpr (BN == 64) {
+    if (cv.MT == 4) return launch_conv<BN, R, KT, 4>(cv, x, s);
     if (cv.MT == 2) return launch_conv<BN, R, KT, 2>(cv, x, s);
   }
   return launch_conv<BN, R, KT, 1>(cv, x, s);
