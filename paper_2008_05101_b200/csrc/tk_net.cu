@@ -307,12 +307,16 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
           }
           const uint32_t at = a0 + (toff[t] >> 4);
           if (do_mma) {
+            if constexpr (MT <= 2)
+              sm100::mma_tap_elect<kSteps, MT>(d, at, b0, dhi, idesc, (ci | t) != 0, (uint32_t)(128 * R / 16),
+                                               (uint32_t)BN);
+            else
 #pragma unroll
-            for (int k = 0; k < kSteps; ++k)
+              for (int k = 0; k < kSteps; ++k)
 #pragma unroll
-              for (int u = 0; u < MT; ++u)
-                sm100::mma_i8_elect_lohi(d + u * BN, at + (uint32_t)((u * 128 * R + k * 32) >> 4), dhi,
-                                         b0 + (uint32_t)(k * 2), dhi, idesc, (ci | t | k) != 0);
+                for (int u = 0; u < MT; ++u)
+                  sm100::mma_i8_elect_lohi(d + u * BN, at + (uint32_t)((u * 128 * R + k * 32) >> 4), dhi,
+                                           b0 + (uint32_t)(k * 2), dhi, idesc, (ci | t | k) != 0);
           }
           if (!p.resident) {
             sm100::mma_commit_elect(&w_empty[ws_i]);

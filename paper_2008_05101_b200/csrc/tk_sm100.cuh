@@ -209,6 +209,100 @@ __device__ __forceinline__ void mma_i8_elect_lohi(uint32_t d_tmem, uint32_t a_lo
       "}\n" ::"r"(d_tmem),
       "r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(accumulate));
 }
+// All MMAs of one conv tap in one asm block: kSteps K=32 slices x MT M-tiles,
+// one elect.sync, descriptor low halves advanced with uniform adds (the
+// operands are converted to uniform registers once per tap, not per MMA).
+// A advances 2 (16-byte units) per K slice and aU per M tile; B 2 per K
+// slice; D by dU columns per M tile.  The first K slice of each M tile uses
+// `accumulate`, the later ones always accumulate.
+template <int KS, int MT>
+__device__ __forceinline__ void mma_tap_elect(uint32_t d, uint32_t a_lo, uint32_t b_lo, uint32_t hi, uint32_t idesc,
+                                              uint32_t accumulate, uint32_t aU, uint32_t dU);
+#define TK_MMA1(DREG, AREG, BREG, PRED) \
+  "mov.b64 da, {" AREG ", %3};\n"       \
+  "mov.b64 db, {" BREG ", %3};\n"       \
+  "@e tcgen05.mma.cta_group::1.kind::i8 [" DREG "], da, db, %4, " PRED ";\n"
+template <>
+__device__ __forceinline__ void mma_tap_elect<2, 1>(uint32_t d, uint32_t a_lo, uint32_t b_lo, uint32_t hi,
+                                                    uint32_t idesc, uint32_t accumulate, uint32_t, uint32_t) {
+  asm volatile(
+      "{\n"
+      ".reg .pred e, p, t;\n"
+      ".reg .b64 da, db;\n"
+      ".reg .b32 a1, b1;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "setp.ne.b32 p, %5, 0;\n"
+      "setp.eq.b32 t, %5, %5;\n"
+      "add.u32 a1, %1, 2;\n"
+      "add.u32 b1, %2, 2;\n" TK_MMA1("%0", "%1", "%2", "p") TK_MMA1("%0", "a1", "b1", "t") "}\n" ::"r"(d),
+      "r"(a_lo), "r"(b_lo), "r"(hi), "r"(idesc), "r"(accumulate));
+}
+template <>
+__device__ __forceinline__ void mma_tap_elect<4, 1>(uint32_t d, uint32_t a_lo, uint32_t b_lo, uint32_t hi,
+                                                    uint32_t idesc, uint32_t accumulate, uint32_t, uint32_t) {
+  asm volatile(
+      "{\n"
+      ".reg .pred e, p, t;\n"
+      ".reg .b64 da, db;\n"
+      ".reg .b32 a1, b1, a2, b2, a3, b3;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "setp.ne.b32 p, %5, 0;\n"
+      "setp.eq.b32 t, %5, %5;\n"
+      "add.u32 a1, %1, 2;\n"
+      "add.u32 b1, %2, 2;\n"
+      "add.u32 a2, %1, 4;\n"
+      "add.u32 b2, %2, 4;\n"
+      "add.u32 a3, %1, 6;\n"
+      "add.u32 b3, %2, 6;\n" TK_MMA1("%0", "%1", "%2", "p") TK_MMA1("%0", "a1", "b1", "t")
+          TK_MMA1("%0", "a2", "b2", "t") TK_MMA1("%0", "a3", "b3", "t") "}\n" ::"r"(d),
+      "r"(a_lo), "r"(b_lo), "r"(hi), "r"(idesc), "r"(accumulate));
+}
+template <>
+__device__ __forceinline__ void mma_tap_elect<2, 2>(uint32_t d, uint32_t a_lo, uint32_t b_lo, uint32_t hi,
+                                                    uint32_t idesc, uint32_t accumulate, uint32_t aU, uint32_t dU) {
+  asm volatile(
+      "{\n"
+      ".reg .pred e, p, t;\n"
+      ".reg .b64 da, db;\n"
+      ".reg .b32 a1, b1, a2, a3, d1;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "setp.ne.b32 p, %5, 0;\n"
+      "setp.eq.b32 t, %5, %5;\n"
+      "add.u32 a1, %1, 2;\n"
+      "add.u32 b1, %2, 2;\n"
+      "add.u32 a2, %1, %6;\n"
+      "add.u32 a3, a2, 2;\n"
+      "add.u32 d1, %0, %7;\n" TK_MMA1("%0", "%1", "%2", "p") TK_MMA1("d1", "a2", "%2", "p")
+          TK_MMA1("%0", "a1", "b1", "t") TK_MMA1("d1", "a3", "b1", "t") "}\n" ::"r"(d),
+      "r"(a_lo), "r"(b_lo), "r"(hi), "r"(idesc), "r"(accumulate), "r"(aU), "r"(dU));
+}
+template <>
+__device__ __forceinline__ void mma_tap_elect<4, 2>(uint32_t d, uint32_t a_lo, uint32_t b_lo, uint32_t hi,
+                                                    uint32_t idesc, uint32_t accumulate, uint32_t aU, uint32_t dU) {
+  asm volatile(
+      "{\n"
+      ".reg .pred e, p, t;\n"
+      ".reg .b64 da, db;\n"
+      ".reg .b32 a1, a2, a3, a4, a5, a6, a7, b1, b2, b3, d1;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "setp.ne.b32 p, %5, 0;\n"
+      "setp.eq.b32 t, %5, %5;\n"
+      "add.u32 a1, %1, 2;\n"
+      "add.u32 a2, %1, 4;\n"
+      "add.u32 a3, %1, 6;\n"
+      "add.u32 a4, %1, %6;\n"
+      "add.u32 a5, a4, 2;\n"
+      "add.u32 a6, a4, 4;\n"
+      "add.u32 a7, a4, 6;\n"
+      "add.u32 b1, %2, 2;\n"
+      "add.u32 b2, %2, 4;\n"
+      "add.u32 b3, %2, 6;\n"
+      "add.u32 d1, %0, %7;\n" TK_MMA1("%0", "%1", "%2", "p") TK_MMA1("d1", "a4", "%2", "p")
+          TK_MMA1("%0", "a1", "b1", "t") TK_MMA1("d1", "a5", "b1", "t") TK_MMA1("%0", "a2", "b2", "t")
+              TK_MMA1("d1", "a6", "b2", "t") TK_MMA1("%0", "a3", "b3", "t") TK_MMA1("d1", "a7", "b3", "t") "}\n" ::"r"(d),
+      "r"(a_lo), "r"(b_lo), "r"(hi), "r"(idesc), "r"(accumulate), "r"(aU), "r"(dU));
+}
+#undef TK_MMA1
 __device__ __forceinline__ void mma_commit_elect(uint64_t* bar) {
   asm volatile(
       "{\n"
