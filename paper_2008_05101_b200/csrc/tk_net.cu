@@ -642,67 +642,107 @@ constexpr int kStemInRows = 2 * kStemRows + 5, kStemInCols = 2 * kStemCols + 6;
 // consecutive words); plane pitch 120 = 8 mod 16 puts the two image rows a
 // warp reads 16 banks apart: conflict-free shared loads
 constexpr int kStemHalf = kStemInCols / 2, kStemPitch = 120;
-constexpr int kStemSmem = (147 * 64 + 3 * kStemInRows * 2 * kStemPitch) * 4;
+
+// Persistent: one CTA per SM loads the weights once and walks (image, row
+// tile) items; the next item's input band streams in with cp.async (zero
+// fill outside the image) while the current one is computed.
+__device__ __forceinline__ void stem_fill_band(float* band, const float* __restrict__ img, int n, int oy0, int H,
+                                               int W) {
+  for (int i = threadIdx.x; i < 3 * kStemInRows * kStemInCols; i += blockDim.x) {
+    const int ci = i / (kStemInRows * kStemInCols);
+    const int r = (i / kStemInCols) % kStemInRows, c = i % kStemInCols;
+    const int y = 2 * oy0 - 3 + r, x = c - 3;
+    const bool in = y >= 0 && y < H && x >= 0 && x < W;
+    const float* src = in ? img + ((size_t)(n * 3 + ci) * H + y) * W + x : img;
+    const uint32_t dst = sm100::smem_u32(band + ((ci * kStemInRows + r) * 2 + (c & 1)) * kStemPitch + (c >> 1));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src), "r"(in ? 4 : 0) : "memory");
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
 
 __global__ void __launch_bounds__(256, 1)
-k_stem_conv(const float* __restrict__ img, const float* __restrict__ wgt, int H, int W, int Ho, int Wo,
+k_stem_conv(const float* __restrict__ img, const float* __restrict__ wgt, int N, int H, int W, int Ho, int Wo,
             float* __restrict__ out) {
   extern __shared__ __align__(16) float s_stem[];
-  float* s_w = s_stem;                 // [tap][cout]
-  float* s_in = s_stem + 147 * 64;     // [ci][row][parity][kStemPitch]
-  const int n = blockIdx.y, oy0 = blockIdx.x * kStemRows;
+  float* s_w = s_stem;                                     // [tap][cout]
+  constexpr int kBand = 3 * kStemInRows * 2 * kStemPitch;  // [ci][row][parity][kStemPitch]
+  float* s_band[2] = {s_stem + 147 * 64, s_stem + 147 * 64 + kBand};
   for (int i = threadIdx.x; i < 147 * 64; i += 256) {
     const int co = i / 147, tap = i - co * 147;  // weights [cout][ci][ky][kx]
     s_w[tap * 64 + co] = __ldg(wgt + i);
   }
-  for (int i = threadIdx.x; i < 3 * kStemInRows * kStemInCols; i += 256) {
-    const int ci = i / (kStemInRows * kStemInCols);
-    const int r = (i / kStemInCols) % kStemInRows, c = i % kStemInCols;
-    const int y = 2 * oy0 - 3 + r, x = c - 3;
-    s_in[((ci * kStemInRows + r) * 2 + (c & 1)) * kStemPitch + (c >> 1)] =
-        (y >= 0 && y < H && x >= 0 && x < W) ? __ldg(img + ((size_t)(n * 3 + ci) * H + y) * W + x) : 0.0f;
-  }
-  __syncthreads();
+  const int tiles = (Ho + kStemRows - 1) / kStemRows, n_items = N * tiles;
+  int item = blockIdx.x;
+  if (item < n_items) stem_fill_band(s_band[0], img, item / tiles, (item % tiles) * kStemRows, H, W);
   const int cg = threadIdx.x >> 6;      // channel group of 16 (warp-uniform)
   const int pg = threadIdx.x & 63;
   const int row = pg >> 4, c0 = pg & 15;  // output columns c0, c0+16, ..., c0+96
-  float acc[16][kStemPx];
+  for (int buf = 0; item < n_items; item += gridDim.x, buf ^= 1) {
+    const int nxt = item + gridDim.x;
+    if (nxt < n_items) {
+      stem_fill_band(s_band[buf ^ 1], img, nxt / tiles, (nxt % tiles) * kStemRows, H, W);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+    const float* s_in = s_band[buf];
+    // packed fp32x2 FMA (FFMA2): channel pairs (c, c+1) per instruction, the
+    // input value broadcast to both halves -- each half is an ordinary
+    // round-to-nearest fp32 FMA, so the results are those of __fmaf_rn
+    unsigned long long acc[8][kStemPx];
 #pragma unroll
-  for (int c = 0; c < 16; ++c)
+    for (int c = 0; c < 8; ++c)
 #pragma unroll
-    for (int j = 0; j < kStemPx; ++j) acc[c][j] = 0.0f;
-  for (int ci = 0; ci < 3; ++ci)
+      for (int j = 0; j < kStemPx; ++j) acc[c][j] = 0ull;
 #pragma unroll 1
-    for (int ky = 0; ky < 7; ++ky) {
-      const float* in_row = s_in + (ci * kStemInRows + 2 * row + ky) * 2 * kStemPitch;
+    for (int ci = 0; ci < 3; ++ci)
 #pragma unroll
-      for (int kx = 0; kx < 7; ++kx) {
-        const float4* w4 = reinterpret_cast<const float4*>(s_w + ((ci * 7 + ky) * 7 + kx) * 64 + cg * 16);
-        float wv[16];
+      for (int ky = 0; ky < 7; ++ky) {
+        const float* in_row = s_in + (ci * kStemInRows + 2 * row + ky) * 2 * kStemPitch;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const float4 t = w4[q];
-          wv[4 * q] = t.x; wv[4 * q + 1] = t.y; wv[4 * q + 2] = t.z; wv[4 * q + 3] = t.w;
+        for (int kx = 0; kx < 7; ++kx) {
+          const ulonglong2* w4 =
+              reinterpret_cast<const ulonglong2*>(s_w + ((ci * 7 + ky) * 7 + kx) * 64 + cg * 16);
+          unsigned long long wv[8];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const ulonglong2 t = w4[q];
+            wv[2 * q] = t.x;
+            wv[2 * q + 1] = t.y;
+          }
+          // input column 2*oc + kx (band coordinates) = plane kx&1, word oc + kx/2
+          const float* pl = in_row + (kx & 1) * kStemPitch + (kx >> 1) + c0;
+          unsigned long long xv[kStemPx];
+#pragma unroll
+          for (int j = 0; j < kStemPx; ++j) {
+            const float x = pl[16 * j];
+            asm("mov.b64 %0, {%1, %1};" : "=l"(xv[j]) : "f"(x));
+          }
+#pragma unroll
+          for (int c = 0; c < 8; ++c)
+#pragma unroll
+            for (int j = 0; j < kStemPx; ++j)
+              asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc[c][j]) : "l"(wv[c]), "l"(xv[j]));
         }
-        // input column 2*oc + kx (band coordinates) = plane kx&1, word oc + kx/2
-        const float* pl = in_row + (kx & 1) * kStemPitch + (kx >> 1) + c0;
-        float xv[kStemPx];
+      }
+    const int n = item / tiles, oy = (item % tiles) * kStemRows + row;
+    if (oy < Ho) {
 #pragma unroll
-        for (int j = 0; j < kStemPx; ++j) xv[j] = pl[16 * j];
+      for (int c = 0; c < 8; ++c) {
+        float* o0 = out + ((size_t)(n * 64 + cg * 16 + 2 * c) * Ho + oy) * Wo;
+        float* o1 = o0 + (size_t)Ho * Wo;
 #pragma unroll
-        for (int c = 0; c < 16; ++c)
-#pragma unroll
-          for (int j = 0; j < kStemPx; ++j) acc[c][j] = __fmaf_rn(wv[c], xv[j], acc[c][j]);
+        for (int j = 0; j < kStemPx; ++j)
+          if (c0 + 16 * j < Wo) {
+            float lo, hi;
+            asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(acc[c][j]));
+            o0[c0 + 16 * j] = lo;
+            o1[c0 + 16 * j] = hi;
+          }
       }
     }
-  const int oy = oy0 + row;
-  if (oy >= Ho) return;
-#pragma unroll
-  for (int c = 0; c < 16; ++c) {
-    float* o = out + ((size_t)(n * 64 + cg * 16 + c) * Ho + oy) * Wo;
-#pragma unroll
-    for (int j = 0; j < kStemPx; ++j)
-      if (c0 + 16 * j < Wo) o[c0 + 16 * j] = acc[c][j];
+    __syncthreads();  // everyone is done with this band before it is refilled
   }
 }
 
@@ -1379,14 +1419,15 @@ int tk_stem_conv7x7s2(tk_context* ctx, const float* images, int n, int h, int w,
   const int ho = (h + 6 - 7) / 2 + 1, wo = (w + 6 - 7) / 2 + 1;
   if (wo > kStemCols || (w + 6) > kStemInCols) return TK_ERR_UNSUPPORTED;  // one CTA spans the width
   if (n == 0) return TK_OK;
-  dim3 grid((ho + kStemRows - 1) / kStemRows, n);
-  const int smem = kStemSmem;
+  const int smem = (147 * 64 + 2 * 3 * kStemInRows * 2 * kStemPitch) * 4;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_stem_conv, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
-  k_stem_conv<<<grid, 256, smem, (cudaStream_t)stream>>>(images, weights, h, w, ho, wo, out);
+  const int items = n * ((ho + kStemRows - 1) / kStemRows);
+  k_stem_conv<<<std::min(items, ctx->num_sms), 256, smem, (cudaStream_t)stream>>>(images, weights, n, h, w, ho, wo,
+                                                                                  out);
   return cudaGetLastError() == cudaSuccess ? TK_OK : TK_ERR_CUDA;
 }
 
