@@ -167,6 +167,20 @@ int tk_fully_connected_ternary(tk_context* ctx, const tk_layer* layer,
                                const float* x, int batch, int mask_mode,
                                float* out, void* stream);
 
+/* ---- packed_forward float pieces (R:tinynet.hpp:713-735, FATN models) ----- */
+/* detail::matmul_t (R:tinynet.hpp, used by packed_forward for stem / head):
+ * y[b][o] = bias[o] + sum_j x[b][j] * w[o][j] with the reference build's
+ * operation order (see oracle/ternkit_oracle.c or_matmul_t); relu != 0 then
+ * applies std::max(v, 0.0f).  Device pointers, w row-major [out_dim][in_dim],
+ * bias may be NULL. */
+int tk_matmul_t(tk_context* ctx, const float* x, const float* w, const float* bias, int batch, int in_dim,
+                int out_dim, int relu, float* y, void* stream);
+/* packed_forward's block tail (R:tinynet.hpp:720-730): z[i] = max(z[i] + id, 0)
+ * with id = fmaf(cal_gain[j], h[i], cal_bias[j]) (calibration present) or
+ * h[i], j = i % hidden; both calibration pointers or neither. */
+int tk_residual_relu_rows(tk_context* ctx, float* z, const float* h, long long count, int hidden,
+                          const float* cal_gain, const float* cal_bias, void* stream);
+
 /* ---- network-level packed inference (R:tinynet.hpp:713-735 pattern) -------
  * A body is a sequence of residual blocks of conv2d_ternary layers (folded BN
  * in each layer's affine): inner convs are followed by ReLU; the last conv's

@@ -209,6 +209,18 @@ def main() -> None:
                                         None, None, head_w, head_b); assert st == 0
     g["pf_logits_nocal"] = logits_nocal
 
+    # ---- FATN model files written by the reference serializer (F2 loader
+    # fixtures, R:model_io.hpp:151-301); its own load_model + packed_forward
+    # reproduce the logits above
+    gdir = os.path.dirname(OUT)
+    os.makedirs(gdir, exist_ok=True)
+    for tag, (c_g, c_b, want) in {"cal": (cg, cb, logits), "nocal": (None, None, logits_nocal)}.items():
+        path = os.path.join(gdir, f"pf_{tag}.fatn")
+        assert R.save_packed_model(path, in_dim, hidden, ncls, stem_w, stem_b, blocks, c_g, c_b, head_w,
+                                   head_b) == 0
+        st, lg = R.load_and_forward(path, xin, batch)
+        assert st == 0 and np.array_equal(lg.view(np.int32), want.view(np.int32))
+
     os.makedirs(os.path.dirname(OUT), exist_ok=True)
     np.savez_compressed(OUT, **g)
     print(f"wrote {OUT}: {len(g)} arrays, {os.path.getsize(OUT) / 1e6:.2f} MB")

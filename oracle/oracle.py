@@ -430,6 +430,26 @@ class Reference:
                                          ptr(a[6], _f32p), ptr(out, _f32p))
         return st, out
 
+    def save_packed_model(self, path, in_dim, hidden, n_classes, stem_w, stem_b, blocks, cal_gain, cal_bias,
+                          head_w, head_b):
+        keep: list = []
+        arr = (NdConv * len(blocks))(*[make_ndconv(b, keep) for b in blocks])
+        a = [np.ascontiguousarray(v, np.float32) if v is not None else None
+             for v in (stem_w, stem_b, cal_gain, cal_bias, head_w, head_b)]
+        f = self.lib.ref_save_packed_model
+        f.argtypes = [C.c_char_p] + [C.c_int] * 3 + [_f32p, _f32p, C.c_int, C.POINTER(NdConv)] + [_f32p] * 4
+        return f(path.encode(), in_dim, hidden, n_classes, ptr(a[0], _f32p), ptr(a[1], _f32p), len(blocks), arr,
+                 ptr(a[2], _f32p), ptr(a[3], _f32p), ptr(a[4], _f32p), ptr(a[5], _f32p))
+
+    def load_and_forward(self, path, x, batch, max_classes=4096):
+        x = np.ascontiguousarray(x, np.float32)
+        out = np.empty(batch * max_classes, np.float32)
+        ncls = C.c_int()
+        f = self.lib.ref_load_and_forward
+        f.argtypes = [C.c_char_p, _f32p, C.c_int, _f32p, C.POINTER(C.c_int)]
+        st = f(path.encode(), ptr(x, _f32p), batch, ptr(out, _f32p), C.byref(ncls))
+        return st, out[: batch * ncls.value].reshape(batch, ncls.value)
+
     def net_create(self, blocks):
         keep: list = []
         arr = make_ndblocks(blocks, keep)

@@ -20,6 +20,7 @@
 #include "ternkit/bitkernels.hpp"
 #include "ternkit/codec.hpp"
 #include "ternkit/linalg.hpp"
+#include "ternkit/model_io.hpp"
 #include "ternkit/quantizer.hpp"
 #include "ternkit/tinynet.hpp"
 
@@ -274,6 +275,48 @@ int ref_packed_forward(const float* x, int batch, int in_dim, int hidden,
     std::vector<float> r = packed_forward(
         m, std::span<const float>(x, static_cast<std::size_t>(batch) * in_dim), batch);
     std::memcpy(logits, r.data(), r.size() * 4);
+  });
+}
+
+// The same model written as a FATN file by the reference's own serializer
+// (R:model_io.hpp:151-207), for the loader fixtures of tests/golden.
+int ref_save_packed_model(const char* path, int in_dim, int hidden, int n_classes, const float* stem_w,
+                          const float* stem_b, int n_blocks, const nd_conv* blocks, const float* cal_gain,
+                          const float* cal_bias, const float* head_w, const float* head_b) {
+  return guard([&] {
+    PackedModel m;
+    m.in_dim = in_dim;
+    m.hidden = hidden;
+    m.n_classes = n_classes;
+    m.stem_w.assign(stem_w, stem_w + static_cast<std::size_t>(hidden) * in_dim);
+    m.stem_b.assign(stem_b, stem_b + hidden);
+    m.head_w.assign(head_w, head_w + static_cast<std::size_t>(n_classes) * hidden);
+    m.head_b.assign(head_b, head_b + n_classes);
+    for (int i = 0; i < n_blocks; ++i) {
+      PackedBlock pb;
+      pb.layer = build_layer(blocks[i]);
+      if (cal_gain) {
+        pb.has_calibration = true;
+        pb.cal_gain.assign(cal_gain + static_cast<std::size_t>(i) * hidden,
+                           cal_gain + static_cast<std::size_t>(i + 1) * hidden);
+        pb.cal_bias.assign(cal_bias + static_cast<std::size_t>(i) * hidden,
+                           cal_bias + static_cast<std::size_t>(i + 1) * hidden);
+      }
+      m.blocks.push_back(std::move(pb));
+    }
+    save_model(m, path);
+  });
+}
+
+// load_model + packed_forward with the reference's own code (R:model_io.hpp:
+// 209-301, R:tinynet.hpp:713-735)
+int ref_load_and_forward(const char* path, const float* x, int batch, float* logits, int* n_classes) {
+  return guard([&] {
+    PackedModel m = load_model(path);
+    std::vector<float> r = packed_forward(m, std::span<const float>(x, static_cast<std::size_t>(batch) * m.in_dim),
+                                          batch);
+    std::memcpy(logits, r.data(), r.size() * 4);
+    *n_classes = m.n_classes;
   });
 }
 

@@ -68,6 +68,8 @@ SIGNATURES = {
     "tk_net_is_fused": (_i, [_vp]),
     "tk_net_forward": (_i, [_vp, _vp, _vp, _vp, _vp, _vp]),
     "tk_affine_relu_maxpool": (_i, [_vp, _vp] + [_i] * 4 + [_vp, _vp, _vp, _vp]),
+    "tk_matmul_t": (_i, [_vp, _vp, _vp, _vp, _i, _i, _i, _i, _vp, _vp]),
+    "tk_residual_relu_rows": (_i, [_vp, _vp, _vp, C.c_longlong, _i, _vp, _vp, _vp]),
     "tk_stem_conv7x7s2": (_i, [_vp, _vp, _i, _i, _i, _vp, _vp, _vp]),
     "tk_net_launches": (_i, [_vp, _i, _i]),
     "tk_net_num_convs": (_i, [_vp]),

@@ -1,0 +1,88 @@
+// tk_mlp.cu -- the float pieces of the reference's packed_forward
+// (R:tinynet.hpp:713-735) for the FATN models: the stem / head dense layers
+// (detail::matmul_t) and the per-block calibrated skip-add + ReLU.
+//
+// Exactness: both follow the reference build's arithmetic operation by
+// operation (oracle/ternkit_oracle.c or_matmul_t / or_residual_relu_rows,
+// pinned against the compiled reference by tests/golden).  nvcc would
+// contract a*b + c into an FMA, so every multiply / add is an explicit
+// round-to-nearest intrinsic.
+#include "tk_internal.cuh"
+
+namespace {
+
+// y[b][o] = bias[o] + sum_j x[b][j] * w[o][j] in the reference build's order:
+// the first n8 + (4 if >= 4 remain) terms are product-rounded then added one
+// by one (GCC's vectorized reduction keeps the sequential order here), the
+// scalar tail is FMA-contracted.  One thread per output.
+__global__ void k_matmul_t(const float* __restrict__ x, const float* __restrict__ w,
+                           const float* __restrict__ bias, int batch, int in_dim, int out_dim,
+                           float* __restrict__ y) {
+  const int n8 = in_dim / 8 * 8;
+  const int nv = n8 + ((in_dim - n8) >= 4 ? 4 : 0);
+  const long long total = (long long)batch * out_dim;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int b = (int)(i / out_dim), o = (int)(i - (long long)b * out_dim);
+    const float* xr = x + (size_t)b * in_dim;
+    const float* wr = w + (size_t)o * in_dim;
+    float acc = bias ? __ldg(bias + o) : 0.0f;
+    for (int j = 0; j < nv; ++j) acc = __fadd_rn(acc, __fmul_rn(__ldg(xr + j), __ldg(wr + j)));
+    for (int j = nv; j < in_dim; ++j) acc = __fmaf_rn(__ldg(xr + j), __ldg(wr + j), acc);
+    y[i] = acc;
+  }
+}
+
+// z[i] = max(z[i] + (cal ? fmaf(cal_gain[j], h[i], cal_bias[j]) : h[i]), 0),
+// j = i % hidden (R:tinynet.hpp:720-730; std::max keeps -0.0)
+__global__ void k_residual_relu_rows(float* __restrict__ z, const float* __restrict__ h, long long count,
+                                     int hidden, const float* __restrict__ cal_gain,
+                                     const float* __restrict__ cal_bias) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int j = (int)(i % hidden);
+    const float id = cal_gain ? __fmaf_rn(__ldg(cal_gain + j), h[i], __ldg(cal_bias + j)) : h[i];
+    const float v = __fadd_rn(z[i], id);
+    z[i] = v < 0.0f ? 0.0f : v;
+  }
+}
+
+// in-place ReLU with the reference's std::max(v, 0.0f) semantics
+__global__ void k_relu(float* __restrict__ z, long long count) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count;
+       i += (long long)gridDim.x * blockDim.x) {
+    const float v = z[i];
+    z[i] = v < 0.0f ? 0.0f : v;
+  }
+}
+
+unsigned grid_of(long long work) {
+  const long long g = (work + 255) / 256;
+  return (unsigned)(g < 1 ? 1 : (g > 148 * 32 ? 148 * 32 : g));
+}
+
+}  // namespace
+
+extern "C" {
+
+int tk_matmul_t(tk_context* ctx, const float* x, const float* w, const float* bias, int batch, int in_dim,
+                int out_dim, int relu, float* y, void* stream) {
+  if (!ctx || !x || !w || !y || batch < 0 || in_dim <= 0 || out_dim <= 0) return TK_ERR_INVALID;
+  const long long total = (long long)batch * out_dim;
+  if (total == 0) return TK_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  k_matmul_t<<<grid_of(total), 256, 0, s>>>(x, w, bias, batch, in_dim, out_dim, y);
+  if (relu) k_relu<<<grid_of(total), 256, 0, s>>>(y, total);
+  return cudaGetLastError() == cudaSuccess ? TK_OK : TK_ERR_CUDA;
+}
+
+int tk_residual_relu_rows(tk_context* ctx, float* z, const float* h, long long count, int hidden,
+                          const float* cal_gain, const float* cal_bias, void* stream) {
+  if (!ctx || !z || !h || count < 0 || hidden <= 0 || count % hidden) return TK_ERR_INVALID;
+  if ((cal_gain == nullptr) != (cal_bias == nullptr)) return TK_ERR_INVALID;
+  if (count == 0) return TK_OK;
+  k_residual_relu_rows<<<grid_of(count), 256, 0, (cudaStream_t)stream>>>(z, h, count, hidden, cal_gain, cal_bias);
+  return cudaGetLastError() == cudaSuccess ? TK_OK : TK_ERR_CUDA;
+}
+
+}  // extern "C"

@@ -38,6 +38,12 @@ __global__ void __launch_bounds__(192, 1) k(const __grid_constant__ CUtensorMap 
       sm100::mbar_wait(&bar[i], 0);
     }
   }
+  if (V >= 7 && sink[0] == 0x7fffffff) {  // large, never-executed body: instruction-cache footprint
+    float a = threadIdx.x;
+#pragma unroll
+    for (int i = 0; i < 3000; ++i) a = __fmaf_rn(a, 1.0001f, (float)i);
+    sink[1] = (int)a;
+  }
   if (threadIdx.x == 0 && sink[blockIdx.x] == 12345) sink[0] = smem[0];
   if (V >= 3) {
     __syncthreads();
@@ -96,6 +102,7 @@ int main() {
   printf("+ tensormap prefetch:           %.2f us/launch\n", run<5>(sink, 200 * 1024, 4));
   printf("+ 8 empty commit round trips:   %.2f us/launch\n", run<6>(sink, 200 * 1024, 4));
   printf("V6 with 225 KB smem:            %.2f us/launch\n", run<6>(sink, 225 * 1024, 4));
+  printf("V6 + 48 KB of (dead) code:      %.2f us/launch\n", run<7>(sink, 225 * 1024, 4));
   printf("err: %s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
 }
