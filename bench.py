@@ -342,6 +342,29 @@ class DotWorkload:
     def e2e_bytes(self):
         return self.x_host.numel() * 8 * 2 + self.P * 8, self.P * 8
 
+    def baselines(self) -> dict:
+        """The paper's comparison kernels on the same pairs (R:bitkernels.hpp:99-224,
+        Tables S1/S2): binary XNOR-popcount (1 bit/elem) and the 2-bit
+        bit-plane decomposition (M = K = 2 planes, 4 binary dots per pair)."""
+        import torch
+        tk, P, N = self.tk, self.P, self.N
+        g = torch.Generator(device="cuda").manual_seed(7)
+        words = (N + 63) // 64
+        bx = torch.randint(-2**62, 2**62, (P, words), generator=g, device="cuda")
+        by = torch.randint(-2**62, 2**62, (P, words), generator=g, device="cuda")
+        px = torch.randint(-2**62, 2**62, (2, P, words), generator=g, device="cuda")
+        py = torch.randint(-2**62, 2**62, (2, P, words), generator=g, device="cuda")
+        flush = L2Flush()
+        t_bin = _time_graph(graph_of(lambda: tk.binary_dot_batched(bx, by, N)), flush)
+        sc = torch.tensor([1.0, 2.0], dtype=torch.float64, device="cuda")
+        t_mb = _time_graph(graph_of(lambda: tk.multibit_dot_batched(px, sc, py, sc, N)), flush)
+        t_ter = _time_graph(graph_of(self.step), flush)
+        ops = 2.0 * P * N / 1e12
+        return {"ternary_tops": round(ops / (t_ter / 1e3), 3), "binary_tops": round(ops / (t_bin / 1e3), 3),
+                "multibit2_tops": round(ops / (t_mb / 1e3), 3),
+                "ternary_speedup_vs_2bit": round(t_mb / t_ter, 3), "binary_speedup_vs_ternary": round(t_ter / t_bin, 3),
+                "note": "L2 flushed before each; ops = 2*N*pairs for all three"}
+
     def roofline(self, flush) -> dict:
         ms = _time_graph(graph_of(self.step), flush)
         return {"kernel": "k_dot_batched (LOP3 + POPC, warp per pair)", "bound": "hbm",
@@ -535,6 +558,8 @@ def run_ours(args) -> None:
     e2e_value = job_units / (ems / 1e3)
     # ---- roofline of the dominant kernel ----
     r = w.roofline(flush)
+    if hasattr(w, "baselines") and rank == 0:
+        w.config["paper_baselines"] = w.baselines()
     peaks = load_peaks()
     if r["bound"] == "tensor":
         peak, psrc = peaks["i8_tc_tops"], "measured int8 tensor GEMM, cuBLASLt via torch._int_mm (profiles/peaks_r01.json)"

@@ -167,6 +167,21 @@ int tk_fully_connected_ternary(tk_context* ctx, const tk_layer* layer,
                                const float* x, int batch, int mask_mode,
                                float* out, void* stream);
 
+/* ---- paper baselines: binary and bit-plane multi-bit dots (F3) ----------- */
+/* pack_binary(span<const int8_t>) (R:bitkernels.hpp:170-182): +1 -> bit 1,
+ * -1 -> bit 0, little-endian, zero-padded; other values raise TK_ERR_RANGE
+ * at the next tk_context_sync.  words: (n + 63) / 64 u64. */
+int tk_pack_binary(tk_context* ctx, const int8_t* values, size_t n, uint64_t* words, void* stream);
+/* binary_dot (R:bitkernels.hpp:99-110, 184-191), batched: x, y [pairs][words] */
+int tk_binary_dot_batched(tk_context* ctx, const uint64_t* x, const uint64_t* y, size_t words, size_t logical_len,
+                          size_t pairs, int64_t* out, void* stream);
+/* multibit_dot (R:bitkernels.hpp:196-222), batched: x_planes [m][pairs][words],
+ * y_planes [k][pairs][words], f64 scales; the f64 accumulation follows the
+ * reference's (m, k) order and roundings, so results are bit-identical */
+int tk_multibit_dot_batched(tk_context* ctx, const uint64_t* x_planes, int m, const uint64_t* y_planes, int k,
+                            const double* x_scales, const double* y_scales, size_t words, size_t logical_len,
+                            size_t pairs, double* out, void* stream);
+
 /* ---- packed_forward float pieces (R:tinynet.hpp:713-735, FATN models) ----- */
 /* detail::matmul_t (R:tinynet.hpp, used by packed_forward for stem / head):
  * y[b][o] = bias[o] + sum_j x[b][j] * w[o][j] with the reference build's

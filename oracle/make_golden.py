@@ -209,6 +209,30 @@ def main() -> None:
                                         None, None, head_w, head_b); assert st == 0
     g["pf_logits_nocal"] = logits_nocal
 
+    # ---- paper baselines: binary (Eq. 1) and bit-plane multi-bit (Eq. 2) --------
+    # (R:bitkernels.hpp:99-224; cases after R:tests/test_bitkernels.cpp:157-220,
+    # R:tests/acceptance.cpp:94-117)
+    bin_lens = [8, 1, 63, 64, 65, 700, 4096]
+    for i, n in enumerate(bin_lens):
+        bx = rng.choice(np.array([-1, 1], np.int8), n)
+        by = rng.choice(np.array([-1, 1], np.int8), n)
+        st, wx = R.pack_binary(bx); assert st == 0
+        st, wy = R.pack_binary(by); assert st == 0
+        st, d = R.binary_dot(wx, wy, n); assert st == 0 and d == int(bx.astype(np.int64) @ by)
+        g.update({f"bin{i}_x": bx, f"bin{i}_y": by, f"bin{i}_wx": wx, f"bin{i}_wy": wy,
+                  f"bin{i}_dot": np.array([d], np.int64)})
+    mb = []
+    for i, (n, m, k) in enumerate([(100, 2, 2), (4096, 2, 2), (333, 3, 1), (64, 1, 3)]):
+        xs = [rng.choice(np.array([-1, 1], np.int8), n) for _ in range(m)]
+        ys = [rng.choice(np.array([-1, 1], np.int8), n) for _ in range(k)]
+        sx = (np.array([1.0, 2.0, 4.0])[:m] if i < 2 else rng.standard_normal(m)).astype(np.float64)
+        sy = (np.array([1.0, 2.0, 4.0])[:k] if i < 2 else rng.standard_normal(k)).astype(np.float64)
+        xp = np.stack([R.pack_binary(v)[1] for v in xs])
+        yp = np.stack([R.pack_binary(v)[1] for v in ys])
+        st, d = R.multibit_dot(xp, sx, yp, sy, n); assert st == 0
+        g.update({f"mb{i}_xp": xp, f"mb{i}_yp": yp, f"mb{i}_sx": sx, f"mb{i}_sy": sy,
+                  f"mb{i}_dims": np.array([n, m, k], np.int64), f"mb{i}_dot": np.array([d], np.float64)})
+
     # ---- FATN model files written by the reference serializer (F2 loader
     # fixtures, R:model_io.hpp:151-301); its own load_model + packed_forward
     # reproduce the logits above

@@ -116,6 +116,33 @@ class Oracle:
                                   C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)]
         L.or_matmul_t.argtypes = [_f32p, _f32p, _f32p, C.c_int, C.c_int, C.c_int, _f32p]
         L.or_matmul_t.restype = None
+        L.or_pack_binary.argtypes = [_i8p, _sz, _u64p]
+        L.or_binary_dot.argtypes = [_u64p, _u64p, _sz, _sz]
+        L.or_binary_dot.restype = C.c_int64
+        L.or_multibit_dot.argtypes = [_u64p, C.c_int, _u64p, C.c_int, C.POINTER(C.c_double),
+                                      C.POINTER(C.c_double), _sz, _sz, C.c_int]
+        L.or_multibit_dot.restype = C.c_double
+
+    # paper baselines (R:bitkernels.hpp:99-224) ----------------------------
+    def pack_binary(self, v):
+        v = np.ascontiguousarray(v, dtype=np.int8)
+        w = np.zeros((v.size + 63) // 64, np.uint64)
+        st = self.lib.or_pack_binary(ptr(v, _i8p), v.size, ptr(w, _u64p))
+        return st, w
+
+    def binary_dot(self, x, y, n):
+        x = np.ascontiguousarray(x, np.uint64)
+        y = np.ascontiguousarray(y, np.uint64)
+        return self.lib.or_binary_dot(ptr(x, _u64p), ptr(y, _u64p), x.size, n)
+
+    def multibit_dot(self, xp, sx, yp, sy, n):
+        xp = np.ascontiguousarray(xp, np.uint64)
+        yp = np.ascontiguousarray(yp, np.uint64)
+        sx = np.ascontiguousarray(sx, np.float64)
+        sy = np.ascontiguousarray(sy, np.float64)
+        dp = C.POINTER(C.c_double)
+        return self.lib.or_multibit_dot(ptr(xp, _u64p), xp.shape[0], ptr(yp, _u64p), yp.shape[0],
+                                        sx.ctypes.data_as(dp), sy.ctypes.data_as(dp), xp.shape[1], n, 0)
 
     # scalar quantizers -------------------------------------------------
     def quantize_weight_value(self, p, a1, a2):
@@ -429,6 +456,35 @@ class Reference:
                                          ptr(a[3], _f32p), ptr(a[4], _f32p), ptr(a[5], _f32p),
                                          ptr(a[6], _f32p), ptr(out, _f32p))
         return st, out
+
+    def pack_binary(self, v):
+        v = np.ascontiguousarray(v, dtype=np.int8)
+        w = np.zeros((v.size + 63) // 64, np.uint64)
+        f = self.lib.ref_pack_binary
+        f.argtypes = [_i8p, _sz, _u64p]
+        return f(ptr(v, _i8p), v.size, ptr(w, _u64p)), w
+
+    def binary_dot(self, x, y, n):
+        x = np.ascontiguousarray(x, np.uint64)
+        y = np.ascontiguousarray(y, np.uint64)
+        out = C.c_int64()
+        f = self.lib.ref_binary_dot
+        f.argtypes = [_u64p, _u64p, _sz, _sz, _i64p]
+        st = f(ptr(x, _u64p), ptr(y, _u64p), x.size, n, C.byref(out))
+        return st, out.value
+
+    def multibit_dot(self, xp, sx, yp, sy, n):
+        xp = np.ascontiguousarray(xp, np.uint64)
+        yp = np.ascontiguousarray(yp, np.uint64)
+        sx = np.ascontiguousarray(sx, np.float64)
+        sy = np.ascontiguousarray(sy, np.float64)
+        dp = C.POINTER(C.c_double)
+        out = C.c_double()
+        f = self.lib.ref_multibit_dot
+        f.argtypes = [_u64p, C.c_int, _u64p, C.c_int, dp, dp, _sz, _sz, dp]
+        st = f(ptr(xp, _u64p), xp.shape[0], ptr(yp, _u64p), yp.shape[0], sx.ctypes.data_as(dp),
+               sy.ctypes.data_as(dp), xp.shape[1], n, C.byref(out))
+        return st, out.value
 
     def save_packed_model(self, path, in_dim, hidden, n_classes, stem_w, stem_b, blocks, cal_gain, cal_bias,
                           head_w, head_b):

@@ -320,6 +320,47 @@ int ref_load_and_forward(const char* path, const float* x, int batch, float* log
   });
 }
 
+// ---- paper baselines (R:bitkernels.hpp:99-224) ----
+int ref_pack_binary(const std::int8_t* v, std::size_t n, std::uint64_t* words) {
+  return guard([&] {
+    PackedBinaryVector p = pack_binary(std::span<const std::int8_t>(v, n));
+    std::memcpy(words, p.words.data(), p.words.size() * 8);
+  });
+}
+
+int ref_binary_dot(const std::uint64_t* x, const std::uint64_t* y, std::size_t words, std::size_t logical_len,
+                   std::int64_t* out) {
+  return guard([&] {
+    PackedBinaryVector a, b;
+    a.words.assign(x, x + words);
+    b.words.assign(y, y + words);
+    a.logical_len = b.logical_len = logical_len;
+    *out = binary_dot(a, b);
+  });
+}
+
+int ref_multibit_dot(const std::uint64_t* x, int m, const std::uint64_t* y, int k, const double* sx,
+                     const double* sy, std::size_t words, std::size_t logical_len, double* out) {
+  return guard([&] {
+    MultiBitVector a, b;
+    for (int i = 0; i < m; ++i) {
+      PackedBinaryVector p;
+      p.words.assign(x + i * words, x + (i + 1) * words);
+      p.logical_len = logical_len;
+      a.planes.push_back(std::move(p));
+      a.scales.push_back(sx[i]);
+    }
+    for (int i = 0; i < k; ++i) {
+      PackedBinaryVector p;
+      p.words.assign(y + i * words, y + (i + 1) * words);
+      p.logical_len = logical_len;
+      b.planes.push_back(std::move(p));
+      b.scales.push_back(sy[i]);
+    }
+    *out = multibit_dot(a, b);
+  });
+}
+
 // ---- network body (ResNet-shaped residual blocks) ----
 
 void* ref_net_create(const nd_block* blocks, int n_blocks) {

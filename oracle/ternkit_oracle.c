@@ -355,3 +355,32 @@ void or_matmul_t(const float* x, const float* w, const float* bias, int batch,
       y[(size_t)b * out_dim + o] = acc;
     }
 }
+
+/* ---- paper baselines (R:bitkernels.hpp:99-224) ---------------------------- */
+int or_pack_binary(const int8_t* v, size_t n, uint64_t* words) {
+  const size_t nw = (n + 63) / 64;
+  for (size_t i = 0; i < nw; ++i) words[i] = 0;
+  for (size_t i = 0; i < n; ++i) {
+    if (v[i] != 1 && v[i] != -1) return OR_ERR_INVALID;
+    if (v[i] == 1) words[i / 64] |= 1ull << (i % 64);
+  }
+  return OR_OK;
+}
+
+int64_t or_binary_dot(const uint64_t* x, const uint64_t* y, size_t words, size_t logical_len) {
+  int64_t pop = 0;
+  for (size_t i = 0; i < words; ++i) pop += __builtin_popcountll(~(x[i] ^ y[i]));
+  return 2 * pop - 2 * (int64_t)words * 64 + (int64_t)logical_len;
+}
+
+double or_multibit_dot(const uint64_t* x, int m, const uint64_t* y, int k, const double* sx,
+                       const double* sy, size_t words, size_t logical_len, int contract) {
+  double acc = 0.0;
+  for (int a = 0; a < m; ++a)
+    for (int b = 0; b < k; ++b) {
+      const double bd = (double)or_binary_dot(x + (size_t)a * words, y + (size_t)b * words, words, logical_len);
+      const double s = sx[a] * sy[b];
+      acc = contract ? fma(s, bd, acc) : acc + s * bd;
+    }
+  return acc;
+}

@@ -88,6 +88,18 @@ int or_net_body(const nd_block* blocks, int n_blocks, const float* x, int n,
 void or_matmul_t(const float* x, const float* w, const float* bias, int batch,
                  int in_dim, int out_dim, float* y);
 
+/* ---- paper baselines (R:bitkernels.hpp:99-224) ------------------------- */
+/* pack_binary: +1 -> bit 1, -1 -> bit 0, little-endian, zero-padded; returns
+ * OR_ERR_INVALID for values outside {-1, +1} (R:bitkernels.hpp:170-182) */
+int or_pack_binary(const int8_t* v, size_t n, uint64_t* words);
+/* binary_dot_words (R:bitkernels.hpp:99-110) */
+int64_t or_binary_dot(const uint64_t* x, const uint64_t* y, size_t words, size_t logical_len);
+/* multibit_dot (R:bitkernels.hpp:196-222): planes [m][words], [k][words];
+ * `contract` selects fma(sx*sy, bd, acc) (the reference build's FMA
+ * contraction) over the two-rounding form */
+double or_multibit_dot(const uint64_t* x, int m, const uint64_t* y, int k, const double* sx,
+                       const double* sy, size_t words, size_t logical_len, int contract);
+
 #ifdef __cplusplus
 }
 #endif

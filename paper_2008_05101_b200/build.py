@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libternkit_b200.so")
-SOURCES = ["tk_api.cu", "tk_codec.cu", "tk_popc.cu", "tk_tc.cu", "tk_net.cu", "tk_mlp.cu"]
+SOURCES = ["tk_api.cu", "tk_codec.cu", "tk_popc.cu", "tk_tc.cu", "tk_net.cu", "tk_mlp.cu", "tk_binary.cu"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -238,6 +238,86 @@ def ternary_dot_nonneg(a: PackedTernaryVector, w: PackedTernaryVector, w_sum: in
 
 
 # ---------------------------------------------------------------------------
+# paper baselines (R:bitkernels.hpp:99-224): binary and bit-plane multi-bit dots
+
+
+@dataclass
+class PackedBinaryVector:  # R:bitkernels.hpp:165-168
+    words: torch.Tensor  # int64 view of u64 words (device)
+    logical_len: int
+
+
+def pack_binary(values, check_errors: bool = True) -> PackedBinaryVector:
+    """R:bitkernels.hpp:170-182: values in {-1, +1} only."""
+    v = _dev(values, torch.int8).reshape(-1)
+    n = v.numel()
+    w = torch.empty((n + 63) // 64, dtype=torch.int64, device="cuda")
+    check(T.lib().tk_pack_binary(context(), _p(v), n, _p(w), _stream()), "pack_binary")
+    if check_errors:
+        sync("pack_binary")
+    return PackedBinaryVector(w, n)
+
+
+def binary_dot_batched(x: torch.Tensor, y: torch.Tensor, logical_len: int) -> torch.Tensor:
+    """x, y: [pairs][words] packed binary rows -> int64 [pairs]."""
+    xd, yd = _dev(x, torch.int64), _dev(y, torch.int64)
+    if xd.shape != yd.shape:
+        raise InvalidArgument(T.TK_ERR_INVALID, "binary_dot: length mismatch")
+    pairs, words = xd.shape
+    out = torch.empty(pairs, dtype=torch.int64, device="cuda")
+    check(T.lib().tk_binary_dot_batched(context(), _p(xd), _p(yd), words, logical_len, pairs, _p(out), _stream()),
+          "binary_dot")
+    return out
+
+
+def binary_dot(x: PackedBinaryVector, y: PackedBinaryVector) -> int:
+    """R:bitkernels.hpp:184-191."""
+    if x.logical_len != y.logical_len:
+        raise InvalidArgument(T.TK_ERR_INVALID, "binary_dot: length mismatch")
+    return int(binary_dot_batched(x.words.view(1, -1), y.words.view(1, -1), x.logical_len).item())
+
+
+@dataclass
+class MultiBitVector:  # R:bitkernels.hpp:194-201
+    planes: list
+    scales: list
+
+    def logical_len(self) -> int:
+        return self.planes[0].logical_len if self.planes else 0
+
+
+def multibit_dot_batched(x_planes: torch.Tensor, x_scales, y_planes: torch.Tensor, y_scales,
+                         logical_len: int) -> torch.Tensor:
+    """x_planes [m][pairs][words], y_planes [k][pairs][words] -> f64 [pairs]."""
+    xp, yp = _dev(x_planes, torch.int64), _dev(y_planes, torch.int64)
+    def scales(v):  # host sequences or device f64 tensors (the latter are graph-capturable)
+        if isinstance(v, torch.Tensor) and v.is_cuda:
+            return v.to(torch.float64).contiguous()
+        return torch.as_tensor(np.asarray(v, np.float64)).cuda()
+    sx, sy = scales(x_scales), scales(y_scales)
+    m, pairs, words = xp.shape
+    k = yp.shape[0]
+    if yp.shape[1:] != xp.shape[1:] or sx.numel() != m or sy.numel() != k:
+        raise InvalidArgument(T.TK_ERR_INVALID, "multibit_dot: malformed operand")
+    out = torch.empty(pairs, dtype=torch.float64, device="cuda")
+    check(T.lib().tk_multibit_dot_batched(context(), _p(xp), m, _p(yp), k, _p(sx), _p(sy), words, logical_len,
+                                          pairs, _p(out), _stream()), "multibit_dot")
+    return out
+
+
+def multibit_dot(x: MultiBitVector, y: MultiBitVector) -> float:
+    """R:bitkernels.hpp:196-222 (same validation, bit-identical f64 result)."""
+    if (not x.planes or not y.planes or len(x.planes) != len(x.scales) or len(y.planes) != len(y.scales)):
+        raise InvalidArgument(T.TK_ERR_INVALID, "multibit_dot: malformed operand")
+    n = x.logical_len()
+    if any(p.logical_len != n for p in list(x.planes) + list(y.planes)):
+        raise InvalidArgument(T.TK_ERR_INVALID, "multibit_dot: plane length mismatch")
+    xp = torch.stack([p.words for p in x.planes]).unsqueeze(1)
+    yp = torch.stack([p.words for p in y.planes]).unsqueeze(1)
+    return float(multibit_dot_batched(xp, x.scales, yp, y.scales, n).item())
+
+
+# ---------------------------------------------------------------------------
 # linalg
 
 
