@@ -61,6 +61,9 @@ def load_peaks() -> dict:
     # int8 tensor pipe: measured cuBLASLt int8 GEMM (torch._int_mm) if recorded,
     # else 2x the measured bf16 dense figure (same pipe, twice the rate)
     p.setdefault("i8_tc_tops", 2 * p["bf16_tflops"])
+    # FP4 (kind::mxf4) tensor pipe: twice the int8 rate per SM (measured with
+    # tools/mxf4_test.cu: 16366 vs 8192 MAC/clk/SM), so 2x the measured int8 GEMM
+    p.setdefault("f4_tc_tops", 2 * p["i8_tc_tops"])
     # LOP3+POPC pipe: 16 POPC/clk/SM measured (tools/pipe_bench.cu), 32 ops/POPC
     p.setdefault("popc_tops", 148 * 16 * 32 * p.get("sm_max_mhz", 1965.0) * 1e6 / 1e12)
     return p
@@ -197,8 +200,10 @@ class FcWorkload:
         self.y_pin = torch.empty((batch, cout), dtype=torch.float32).pin_memory()
         self.y = torch.empty((batch, cout), dtype=torch.float32, device="cuda")
         self.x_dev2 = torch.empty_like(self.x)
+        self.backend = self.layer.backend_for(batch)
+        self.fmt = "fp4" if self.backend == tk.Backend.TC_F4 else "s8"
         self.a8 = tk.quantize_levels(self.x, tk.QuantThresholds(0.5, 0.9), tk.QuantMode.kActivationNonneg,
-                                     tk.layer_k_pad(self.layer))
+                                     tk.layer_k_pad(self.layer, self.fmt), self.fmt)
         self.units_per_step = 2.0 * batch * cin * cout / 1e12  # Tera-ops
         self.unit = "Tops/s"
         self.launches_per_step = 2
@@ -234,7 +239,9 @@ class FcWorkload:
             tot += e0.elapsed_time(e1)
         ms = tot / n
         work = 2.0 * self.B * self.C * self.N / 1e12
-        return {"kernel": "ternary GEMM, tcgen05.mma kind::i8 (k_gemm_tc_i8)", "bound": "tensor",
+        kind = "kind::mxf4 (E2M1 levels)" if self.fmt == "fp4" else "kind::i8"
+        return {"kernel": f"ternary GEMM, tcgen05.mma {kind} (k_gemm_tc_i8<BN, {self.fmt == 'fp4'}>)",
+                "bound": "tensor", "pipe": self.fmt,
                 "work": work, "unit": "TFLOP/s", "avg_launch_ms": ms,
                 "algorithmic": f"2*M*N*K = {2 * self.B * self.C * self.N:.4g} int8 ops per launch"}
 
@@ -436,7 +443,7 @@ class ConvWorkload:
         # pipe choice by measurement on this shape
         self.pipe_ms = {}
         flush = L2Flush()
-        for be in (tk.Backend.POPC, tk.Backend.TC_I8):
+        for be in (tk.Backend.POPC, tk.Backend.TC_I8, tk.Backend.TC_F4):
             self.layer.set_backend(be)
             self.pipe_ms[be.name] = _time_graph(graph_of(self.step), flush, n=30)
         best = min(self.pipe_ms, key=self.pipe_ms.get)
@@ -467,9 +474,9 @@ class ConvWorkload:
         launch-latency bound at b1: 231 Mop is ~0.1 us of tensor-pipe work)."""
         ms = _time_graph(graph_of(self.step), flush)
         tk = self.tk
-        bound = "tensor" if self.backend == tk.Backend.TC_I8 else "int"
+        bound = "int" if self.backend == tk.Backend.POPC else "tensor"
         return {"kernel": f"conv2d_ternary step ({self.launches_per_step} launches, {self.backend.name} GEMM)",
-                "bound": bound, "work": self.units_per_step, "unit": "TFLOP/s", "avg_launch_ms": ms,
+                "bound": bound, "pipe": "fp4" if self.backend == tk.Backend.TC_F4 else "s8", "work": self.units_per_step, "unit": "TFLOP/s", "avg_launch_ms": ms,
                 "algorithmic": f"2*M*N*K = {2 * self.M * self.K * self.Nc:.4g} ops per step"}
 
     def verify(self) -> bool:
@@ -561,7 +568,10 @@ def run_ours(args) -> None:
     if hasattr(w, "baselines") and rank == 0:
         w.config["paper_baselines"] = w.baselines()
     peaks = load_peaks()
-    if r["bound"] == "tensor":
+    if r["bound"] == "tensor" and r.get("pipe") == "fp4":
+        peak, psrc = peaks["f4_tc_tops"], ("FP4 tensor pipe: 2x the measured int8 tensor GEMM (kind::mxf4 runs at "
+                                           "2x the kind::i8 MAC rate, tools/mxf4_test.cu)")
+    elif r["bound"] == "tensor":
         peak, psrc = peaks["i8_tc_tops"], "measured int8 tensor GEMM, cuBLASLt via torch._int_mm (profiles/peaks_r01.json)"
     elif r["bound"] == "int":
         peak, psrc = peaks["popc_tops"], "measured POPC pipe x 32 ops (tools/pipe_bench.cu)"

@@ -54,6 +54,8 @@ extern "C" {
 #define TK_BACKEND_AUTO 0    /* per-shape choice (profiles/)       */
 #define TK_BACKEND_POPC 1    /* LOP3 + POPC integer pipe                      */
 #define TK_BACKEND_TC_I8 2   /* tcgen05.mma kind::i8 tensor cores             */
+#define TK_BACKEND_TC_F4 3   /* tcgen05.mma kind::mxf4 (E2M1 levels, unit E8M0
+                                block scales: exact, 2x the i8 MMA rate)       */
 
 typedef struct tk_context tk_context;
 typedef struct tk_layer tk_layer;
@@ -161,6 +163,19 @@ int tk_quantize_levels(tk_context* ctx, const float* x, int rows, int n,
                        float alpha1, float alpha2, int mode, int k_pad,
                        int8_t* out, void* stream);
 int tk_layer_k_pad(const tk_layer* layer);
+/* The same contraction on the FP4 tensor-core path:
+ * levels as E2M1 nibbles (-1 -> 0xA, 0 -> 0x0, 1 -> 0x2, 2 -> 0x4), two per
+ * byte with the even k in the low nibble, K-block-major with 256 levels per
+ * 128-byte block: element (r, k) in byte ((k/256)*m_pad + r)*128 + (k%256)/2.
+ * k_pad = tk_layer_k_pad_fp4 (K rounded up to 256); the operand holds
+ * round_up(rows, 128) * k_pad / 2 bytes.  Results are identical to
+ * tk_gemm_levels (f32 accumulation of integers < 2^24 is exact). */
+int tk_gemm_levels_fp4(tk_context* ctx, const tk_layer* layer, const uint8_t* a_fp4,
+                       int m_rows, int out_mode, void* out, void* stream);
+int tk_quantize_levels_fp4(tk_context* ctx, const float* x, int rows, int n,
+                           float alpha1, float alpha2, int mode, int k_pad,
+                           uint8_t* out, void* stream);
+int tk_layer_k_pad_fp4(const tk_layer* layer);
 
 /* fully_connected_ternary(x, batch, layer, mask_mode) R:linalg.hpp:332-343 */
 int tk_fully_connected_ternary(tk_context* ctx, const tk_layer* layer,
@@ -256,8 +271,10 @@ int tk_net_conv_times(tk_net* net, float* ms_host, double* macs_host);
 /* diagnostics: per-CTA phase stamps of the last conv run with TK_CONV_DBG&16
  * (148*8 + 8*32 u64) */
 int tk_debug_conv_stamps(unsigned long long* host_out);
-/* profiling: per-CTA globaltimer stamps of the last tensor-core GEMM launched
- * with env TK_GEMM_DBG & 16 (grid-linear CTA id < 512, 8 u64 each) */
+/* profiling: per-CTA stamps of the last tensor-core GEMM launched with env
+ * TK_GEMM_DBG & 16 (grid-linear CTA id < 512): [512][8] SM-clock phase
+ * stamps, [2][512][2] globaltimer ns at CTA start / end for the last
+ * launch of each parity, then [512][16] reduction sub-phase stamps (14336 u64) */
 int tk_debug_gemm_stamps(unsigned long long* host_out);
 
 #ifdef __cplusplus

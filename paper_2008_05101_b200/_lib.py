@@ -30,6 +30,7 @@ TK_MASK_PRECOMPUTED = 1
 TK_BACKEND_AUTO = 0
 TK_BACKEND_POPC = 1
 TK_BACKEND_TC_I8 = 2
+TK_BACKEND_TC_F4 = 3
 
 _vp = C.c_void_p
 _sz = C.c_size_t
@@ -62,6 +63,9 @@ SIGNATURES = {
     "tk_gemm_levels": (_i, [_vp, _vp, _vp, _i, _i, _vp, _vp]),
     "tk_quantize_levels": (_i, [_vp, _vp, _i, _i, _f, _f, _i, _i, _vp, _vp]),
     "tk_layer_k_pad": (_i, [_vp]),
+    "tk_gemm_levels_fp4": (_i, [_vp, _vp, _vp, _i, _i, _vp, _vp]),
+    "tk_quantize_levels_fp4": (_i, [_vp, _vp, _i, _i, _f, _f, _i, _i, _vp, _vp]),
+    "tk_layer_k_pad_fp4": (_i, [_vp]),
     "tk_net_create": (_i, [_vp, _vp, _i, _i, _i, _i, _i, _i, C.POINTER(_vp)]),
     "tk_net_destroy": (_i, [_vp]),
     "tk_net_out_shape": (_i, [_vp, C.POINTER(_i), C.POINTER(_i), C.POINTER(_i)]),

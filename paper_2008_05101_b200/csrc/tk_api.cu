@@ -254,6 +254,8 @@ int tk_layer_create(tk_context* ctx, const int8_t* weights_host, int in_c,
   const int k_pad = ((K + 127) / 128) * 128;
   const int n_pad = ((out_c + 255) / 256) * 256;
   std::vector<int8_t> w8((size_t)n_pad * k_pad, 0);
+  const int k_pad4 = ((K + 255) / 256) * 256;
+  std::vector<uint8_t> w4((size_t)n_pad * k_pad4 / 2, 0);  // E2M1 nibbles, even lane low
   for (int o = 0; o < out_c; ++o) {
     int32_t s = 0;
     for (int l = 0; l < K; ++l) {
@@ -264,6 +266,8 @@ int tk_layer_create(tk_context* ctx, const int8_t* weights_host, int in_c,
       wd = (wd & ~(3ull << (2 * (l % 32)))) | (code << (2 * (l % 32)));
       s += v;
       w8[((size_t)(l / 128) * n_pad + o) * 128 + l % 128] = (int8_t)v;  // [k/128][n_pad][128]
+      const uint8_t nib = v < 0 ? 0xA : (v == 0 ? 0x0 : 0x2);            // [k/256][n_pad][128 B]
+      w4[((size_t)(l / 256) * n_pad + o) * 128 + (l % 256) / 2] |= (uint8_t)(nib << (4 * (l & 1)));
     }
     wsum[o] = s;
     int32_t z = 0;
@@ -288,6 +292,7 @@ int tk_layer_create(tk_context* ctx, const int8_t* weights_host, int in_c,
   L->wpr64 = wpr;
   L->k_pad = k_pad;
   L->n_pad = n_pad;
+  L->k_pad4 = k_pad4;
   std::vector<float> gain(out_c, 1.0f), bias(out_c, 0.0f);  // identity, R:linalg.hpp:133
   if (gain_host) memcpy(gain.data(), gain_host, out_c * 4);
   if (bias_host) memcpy(bias.data(), bias_host, out_c * 4);
@@ -298,7 +303,8 @@ int tk_layer_create(tk_context* ctx, const int8_t* weights_host, int in_c,
       cudaMalloc(&L->d_zcnt, out_c * 4) == cudaSuccess &&
       cudaMalloc(&L->d_gain, out_c * 4) == cudaSuccess &&
       cudaMalloc(&L->d_bias, out_c * 4) == cudaSuccess &&
-      cudaMalloc(&L->d_w8, w8.size()) == cudaSuccess;
+      cudaMalloc(&L->d_w8, w8.size()) == cudaSuccess &&
+      cudaMalloc(&L->d_w4, w4.size()) == cudaSuccess;
   if (ok) {
     ok = cudaMemcpy(L->d_words, words.data(), words.size() * 8, cudaMemcpyHostToDevice) == cudaSuccess &&
          cudaMemcpy(L->d_mask, mask.data(), mask.size() * 4, cudaMemcpyHostToDevice) == cudaSuccess &&
@@ -306,7 +312,8 @@ int tk_layer_create(tk_context* ctx, const int8_t* weights_host, int in_c,
          cudaMemcpy(L->d_zcnt, zcnt.data(), out_c * 4, cudaMemcpyHostToDevice) == cudaSuccess &&
          cudaMemcpy(L->d_gain, gain.data(), out_c * 4, cudaMemcpyHostToDevice) == cudaSuccess &&
          cudaMemcpy(L->d_bias, bias.data(), out_c * 4, cudaMemcpyHostToDevice) == cudaSuccess &&
-         cudaMemcpy(L->d_w8, w8.data(), w8.size(), cudaMemcpyHostToDevice) == cudaSuccess;
+         cudaMemcpy(L->d_w8, w8.data(), w8.size(), cudaMemcpyHostToDevice) == cudaSuccess &&
+         cudaMemcpy(L->d_w4, w4.data(), w4.size(), cudaMemcpyHostToDevice) == cudaSuccess;
   }
   L->h_words = (uint64_t*)malloc(words.size() * 8);
   L->h_wsum = (int32_t*)malloc(out_c * 4);
@@ -326,6 +333,7 @@ int tk_layer_destroy(tk_layer* L) {
   cudaFree(L->d_words); cudaFree(L->d_mask); cudaFree(L->d_wsum);
   cudaFree(L->d_zcnt); cudaFree(L->d_gain); cudaFree(L->d_bias);
   cudaFree(L->d_w8);
+  cudaFree(L->d_w4);
   free(L->h_words);
   free(L->h_wsum);
   delete L;
@@ -339,21 +347,32 @@ int tk_layer_precompute_masks(tk_layer* L) {
 }
 
 int tk_layer_set_backend(tk_layer* L, int backend) {
-  if (!L || backend < TK_BACKEND_AUTO || backend > TK_BACKEND_TC_I8)
+  if (!L || backend < TK_BACKEND_AUTO || backend > TK_BACKEND_TC_F4)
     return TK_ERR_INVALID;
   L->backend = backend;
   return TK_OK;
 }
 
 // Per-shape pipe choice (evidence in profiles/):
-// the tensor-core path wins once the tile grid can be filled.
+// the tensor-core path wins once the tile grid can be filled, and there the
+// FP4 operands (half the bytes of s8, twice the MMA rate, same exact sums)
+// beat s8.
 int tk_layer_get_backend(const tk_layer* L, int m_rows) {
   if (!L) return TK_ERR_INVALID;
   if (L->backend != TK_BACKEND_AUTO) return L->backend;
   return tk_tc_supported(m_rows, L->out_c, L->k_pad) && m_rows >= 128
-             ? TK_BACKEND_TC_I8
+             ? TK_BACKEND_TC_F4
              : TK_BACKEND_POPC;
 }
+
+namespace {
+// tensor-core operand format of a backend: fp4 levels or s8 levels
+bool tc_backend(int be) { return be == TK_BACKEND_TC_I8 || be == TK_BACKEND_TC_F4; }
+int tc_k_pad(const tk_layer* L, bool fp4) { return fp4 ? L->k_pad4 : L->k_pad; }
+size_t tc_operand_bytes(const tk_layer* L, size_t m_pad, bool fp4) {
+  return fp4 ? m_pad * L->k_pad4 / 2 : m_pad * L->k_pad;
+}
+}  // namespace
 
 int tk_layer_words_host(const tk_layer* L, uint64_t* words_host,
                         int32_t* wsums_host) {
@@ -374,14 +393,14 @@ int tk_packed_gemm(tk_context* ctx, const tk_layer* L, const uint64_t* rows,
   cudaStream_t s = (cudaStream_t)stream;
   tk_epilogue e{TK_EPI_I32, 1, nullptr, nullptr, 1.0f, out};
   const int be = tk_layer_get_backend(L, (int)row_count);
-  if (be == TK_BACKEND_TC_I8) {
+  if (tc_backend(be)) {
+    const bool f4 = be == TK_BACKEND_TC_F4;
     if (!tk_tc_supported((int)row_count, L->out_c, L->k_pad)) return TK_ERR_UNSUPPORTED;
     const size_t m_pad = (row_count + 127) / 128 * 128;
-    int8_t* a8 = (int8_t*)tk_workspace(ctx, m_pad * L->k_pad);
+    int8_t* a8 = (int8_t*)tk_workspace(ctx, tc_operand_bytes(L, m_pad, f4));
     if (!a8) return TK_ERR_CUDA;
-    TK_CUDA(tk_launch_expand_rows_s8(rows, row_count, L->wpr64, nonneg_offset,
-                                     L->k_pad, a8, s));
-    TK_CUDA(tk_launch_gemm_tc(a8, (int)row_count, L->k_pad, L, e, s));
+    TK_CUDA(tk_launch_expand_rows(rows, row_count, L->wpr64, nonneg_offset, tc_k_pad(L, f4), f4, a8, s));
+    TK_CUDA(tk_launch_gemm_tc_fmt(a8, (int)row_count, tc_k_pad(L, f4), L, e, f4, s));
     return TK_OK;
   }
   TK_CUDA(tk_launch_gemm_popc(rows, row_count, L->wpr64, L, nonneg_offset, e, s));
@@ -409,16 +428,17 @@ int tk_conv2d_ternary(tk_context* ctx, const tk_layer* L, const float* x,
   tk_epilogue e{TK_EPI_F32_NCHW, oh * ow, L->d_gain, L->d_bias, L->out_scale, out};
   const int be = tk_layer_get_backend(L, (int)M);
   const size_t rows_bytes = M * L->wpr64 * 8;
-  if (be == TK_BACKEND_TC_I8 && tk_tc_supported((int)M, L->out_c, L->k_pad)) {
+  if (tc_backend(be) && tk_tc_supported((int)M, L->out_c, L->k_pad)) {
+    const bool f4 = be == TK_BACKEND_TC_F4;
     const size_t m_pad = (M + 127) / 128 * 128;
-    char* ws = (char*)tk_workspace(ctx, rows_bytes + m_pad * L->k_pad + 256);
+    char* ws = (char*)tk_workspace(ctx, rows_bytes + tc_operand_bytes(L, m_pad, f4) + 256);
     if (!ws) return TK_ERR_CUDA;
     uint64_t* rows = (uint64_t*)ws;
     int8_t* a8 = (int8_t*)(ws + ((rows_bytes + 255) / 256) * 256);
     TK_CUDA(tk_launch_im2col(x, n, L->in_c, h, w, L->kh, L->kw, L->stride, L->pad,
                              q, rows, ctx->d_err, s));
-    TK_CUDA(tk_launch_expand_rows_s8(rows, M, L->wpr64, L->nonneg, L->k_pad, a8, s));
-    TK_CUDA(tk_launch_gemm_tc(a8, (int)M, L->k_pad, L, e, s));
+    TK_CUDA(tk_launch_expand_rows(rows, M, L->wpr64, L->nonneg, tc_k_pad(L, f4), f4, a8, s));
+    TK_CUDA(tk_launch_gemm_tc_fmt(a8, (int)M, tc_k_pad(L, f4), L, e, f4, s));
     return TK_OK;
   }
   uint64_t* rows = (uint64_t*)tk_workspace(ctx, rows_bytes);
@@ -430,26 +450,52 @@ int tk_conv2d_ternary(tk_context* ctx, const tk_layer* L, const float* x,
 }
 
 int tk_layer_k_pad(const tk_layer* L) { return L ? L->k_pad : -1; }
+int tk_layer_k_pad_fp4(const tk_layer* L) { return L ? L->k_pad4 : -1; }
 
-int tk_gemm_levels(tk_context* ctx, const tk_layer* L, const int8_t* a_s8, int m_rows,
-                   int out_mode, void* out, void* stream) {
+namespace {
+int gemm_levels(tk_context* ctx, const tk_layer* L, const int8_t* a, int m_rows, int out_mode, void* out,
+                bool fp4, void* stream) {
   if (!ctx || !L || m_rows < 0 || (out_mode != 0 && out_mode != 1)) return TK_ERR_INVALID;
   if (m_rows == 0) return TK_OK;
+  if (!a || !out) return TK_ERR_INVALID;
   if (!tk_tc_supported(m_rows, L->out_c, L->k_pad)) return TK_ERR_UNSUPPORTED;
   tk_epilogue e{out_mode == 0 ? TK_EPI_I32 : TK_EPI_F32_ROWS, 1, L->d_gain, L->d_bias,
                 L->out_scale, out};
-  TK_CUDA(tk_launch_gemm_tc(a_s8, m_rows, L->k_pad, L, e, (cudaStream_t)stream));
+  const cudaError_t ce = tk_launch_gemm_tc_fmt(a, m_rows, tc_k_pad(L, fp4), L, e, fp4, (cudaStream_t)stream);
+  if (ce == cudaErrorNotSupported) return TK_ERR_UNSUPPORTED;
+  TK_CUDA(ce);
   return TK_OK;
+}
+
+int quantize_levels(tk_context* ctx, const float* x, int rows, int n, float a1, float a2, int mode, int k_pad,
+                    bool fp4, int8_t* out, void* stream) {
+  if (!ctx || rows < 0 || n < 0 || k_pad < n || k_pad % (fp4 ? 256 : 128)) return TK_ERR_INVALID;
+  tk_qparams q;
+  const int st = tk_make_qparams(a1, a2, mode, &q);
+  if (st != TK_OK) return st;
+  TK_CUDA(tk_launch_quantize_levels(x, rows, n, q, k_pad, fp4, out, ctx->d_err, (cudaStream_t)stream));
+  return TK_OK;
+}
+}  // namespace
+
+int tk_gemm_levels(tk_context* ctx, const tk_layer* L, const int8_t* a_s8, int m_rows,
+                   int out_mode, void* out, void* stream) {
+  return gemm_levels(ctx, L, a_s8, m_rows, out_mode, out, false, stream);
+}
+
+int tk_gemm_levels_fp4(tk_context* ctx, const tk_layer* L, const uint8_t* a_fp4, int m_rows, int out_mode,
+                       void* out, void* stream) {
+  return gemm_levels(ctx, L, (const int8_t*)a_fp4, m_rows, out_mode, out, true, stream);
 }
 
 int tk_quantize_levels(tk_context* ctx, const float* x, int rows, int n, float a1, float a2,
                        int mode, int k_pad, int8_t* out, void* stream) {
-  if (!ctx || rows < 0 || n < 0 || k_pad < n || k_pad % 128) return TK_ERR_INVALID;
-  tk_qparams q;
-  const int st = tk_make_qparams(a1, a2, mode, &q);
-  if (st != TK_OK) return st;
-  TK_CUDA(tk_launch_quantize_s8(x, rows, n, q, k_pad, out, ctx->d_err, (cudaStream_t)stream));
-  return TK_OK;
+  return quantize_levels(ctx, x, rows, n, a1, a2, mode, k_pad, false, out, stream);
+}
+
+int tk_quantize_levels_fp4(tk_context* ctx, const float* x, int rows, int n, float a1, float a2, int mode,
+                           int k_pad, uint8_t* out, void* stream) {
+  return quantize_levels(ctx, x, rows, n, a1, a2, mode, k_pad, true, (int8_t*)out, stream);
 }
 
 // R:linalg.hpp:332-343: a 1x1, pad-0 conv over [batch][in_c][1][1]
@@ -468,12 +514,13 @@ int tk_fully_connected_ternary(tk_context* ctx, const tk_layer* L,
   cudaStream_t s = (cudaStream_t)stream;
   tk_epilogue e{TK_EPI_F32_ROWS, 1, L->d_gain, L->d_bias, L->out_scale, out};
   const int be = tk_layer_get_backend(L, batch);
-  if (be == TK_BACKEND_TC_I8 && tk_tc_supported(batch, L->out_c, L->k_pad)) {
+  if (tc_backend(be) && tk_tc_supported(batch, L->out_c, L->k_pad)) {
+    const bool f4 = be == TK_BACKEND_TC_F4;
     const size_t m_pad = ((size_t)batch + 127) / 128 * 128;
-    int8_t* a8 = (int8_t*)tk_workspace(ctx, m_pad * L->k_pad);
+    int8_t* a8 = (int8_t*)tk_workspace(ctx, tc_operand_bytes(L, m_pad, f4));
     if (!a8) return TK_ERR_CUDA;
-    TK_CUDA(tk_launch_quantize_s8(x, batch, L->in_c, q, L->k_pad, a8, ctx->d_err, s));
-    TK_CUDA(tk_launch_gemm_tc(a8, batch, L->k_pad, L, e, s));
+    TK_CUDA(tk_launch_quantize_levels(x, batch, L->in_c, q, tc_k_pad(L, f4), f4, a8, ctx->d_err, s));
+    TK_CUDA(tk_launch_gemm_tc_fmt(a8, batch, tc_k_pad(L, f4), L, e, f4, s));
     return TK_OK;
   }
   uint64_t* rows = (uint64_t*)tk_workspace(ctx, (size_t)batch * L->wpr64 * 8);

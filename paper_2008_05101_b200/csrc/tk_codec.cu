@@ -147,16 +147,41 @@ __device__ __forceinline__ uint32_t expand4(uint32_t bits8, uint32_t tbl) {
 // Packed rows -> s8 tensor-core operand [rows][k_pad].  Level = decoded lane
 // value, +1 when the rows carry the nonneg offset (codes -> {0,1,2}), so the
 // integer MMA result equals packed_gemm's offset-corrected dot directly.
+// F4: E2M1 nibbles instead, 16 lanes -> 8 bytes, layout [k/256][m_pad][128 B]
+// with the even lane in the low nibble (the kind::mxf4 operand format).
+__device__ __forceinline__ uint32_t e2m1_of_level(int lv) {  // -1, 0, 1, 2
+  return lv == 0 ? 0x0u : lv == 1 ? 0x2u : lv == 2 ? 0x4u : 0xAu;
+}
+__device__ __forceinline__ void store_chunk_f4(int8_t* out, size_t m_pad, size_t r, int j, uint2 v) {
+  reinterpret_cast<uint2*>(out + ((size_t)(j >> 4) * m_pad + r) * 128)[j & 15] = v;
+}
+
+template <bool F4>
 __global__ void k_expand_rows_s8(const uint32_t* __restrict__ rows,
                                  size_t row_count, int w32pr, int offset,
                                  int k_pad, size_t m_pad, int8_t* __restrict__ out) {
   const int chunks = k_pad / 16;
   const uint32_t tbl = offset ? 0x02010100u : 0x010000FFu;
+  // code -> E2M1 nibble (offset: levels 0,1,1,2; symmetric: -1,0,0,1)
+  const uint32_t ntbl = offset ? 0x4220u : 0x200Au;
   const size_t total = row_count * (size_t)chunks;
   for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total;
        t += (size_t)gridDim.x * blockDim.x) {
     const size_t r = t / chunks;
     const int j = (int)(t - r * chunks);
+    if constexpr (F4) {
+      uint2 o = make_uint2(0, 0);
+      if (j < w32pr) {
+        const uint32_t wd = rows[r * w32pr + j];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const uint32_t nib = (ntbl >> (4 * ((wd >> (2 * i)) & 3u))) & 0xFu;
+          if (i < 8) o.x |= nib << (4 * i); else o.y |= nib << (4 * (i - 8));
+        }
+      }
+      store_chunk_f4(out, m_pad, r, j, o);
+      continue;
+    }
     uint4 o = make_uint4(0, 0, 0, 0);
     if (j < w32pr) {
       const uint32_t wd = rows[r * w32pr + j];
@@ -172,6 +197,7 @@ __global__ void k_expand_rows_s8(const uint32_t* __restrict__ rows,
 
 // Floats -> s8 quantization levels ({0,1,2} activation, {-1,0,1} weight
 // mode) for the tensor-core FC path; columns >= n are zero.
+template <bool F4>
 __global__ void k_quantize_s8(const float* __restrict__ x, size_t rows,
                               size_t n, tk_qparams q, int k_pad, size_t m_pad,
                               int8_t* __restrict__ out,
@@ -199,6 +225,7 @@ __global__ void k_quantize_s8(const float* __restrict__ x, size_t rows,
       for (int i = 0; i < 16; ++i) v[i] = i < valid ? __ldg(src + i) : 0.0f;
     }
     uint32_t b[4] = {0, 0, 0, 0};
+    uint32_t f[2] = {0, 0};  // F4 nibbles
     int first_bad = -1, bad_code = 0;
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
@@ -211,14 +238,21 @@ __global__ void k_quantize_s8(const float* __restrict__ x, size_t rows,
           }
         } else {
           const int lv = (int)(c & 1u) + (int)(c >> 1) + bias;
-          b[i / 4] |= ((uint32_t)(lv & 0xFF)) << (8 * (i % 4));
+          if constexpr (F4)
+            f[i / 8] |= e2m1_of_level(lv) << (4 * (i % 8));
+          else
+            b[i / 4] |= ((uint32_t)(lv & 0xFF)) << (8 * (i % 4));
         }
       }
     }
     if (first_bad >= 0) tk_raise(err, r * n + l0 + first_bad, bad_code);
-    // K-block-major operand layout [k/128][m_pad][128] (contiguous TMA boxes)
-    reinterpret_cast<uint4*>(out + ((size_t)(j >> 3) * m_pad + r) * 128)[j & 7] =
-        make_uint4(b[0], b[1], b[2], b[3]);
+    if constexpr (F4) {
+      store_chunk_f4(out, m_pad, r, j, make_uint2(f[0], f[1]));
+    } else {
+      // K-block-major operand layout [k/128][m_pad][128] (contiguous TMA boxes)
+      reinterpret_cast<uint4*>(out + ((size_t)(j >> 3) * m_pad + r) * 128)[j & 7] =
+          make_uint4(b[0], b[1], b[2], b[3]);
+    }
   }
 }
 
@@ -278,9 +312,14 @@ cudaError_t tk_launch_unpack(const uint64_t* words, size_t n, int8_t* v,
 cudaError_t tk_launch_expand_rows_s8(const uint64_t* rows, size_t row_count,
                                      int wpr64, int offset, int k_pad,
                                      int8_t* out, cudaStream_t s) {
+  return tk_launch_expand_rows(rows, row_count, wpr64, offset, k_pad, false, out, s);
+}
+
+cudaError_t tk_launch_expand_rows(const uint64_t* rows, size_t row_count, int wpr64, int offset, int k_pad,
+                                  bool fp4, int8_t* out, cudaStream_t s) {
   const size_t total = row_count * (size_t)(k_pad / 16);
   if (total == 0) return cudaSuccess;
-  k_expand_rows_s8<<<grid_for(total), kThreads, 0, s>>>(
+  (fp4 ? k_expand_rows_s8<true> : k_expand_rows_s8<false>)<<<grid_for(total), kThreads, 0, s>>>(
       reinterpret_cast<const uint32_t*>(rows), row_count, 2 * wpr64, offset,
       k_pad, (row_count + 127) / 128 * 128, out);
   return cudaGetLastError();
@@ -289,10 +328,15 @@ cudaError_t tk_launch_expand_rows_s8(const uint64_t* rows, size_t row_count,
 cudaError_t tk_launch_quantize_s8(const float* x, size_t rows, size_t n,
                                   tk_qparams q, int k_pad, int8_t* out,
                                   unsigned long long* err, cudaStream_t s) {
+  return tk_launch_quantize_levels(x, rows, n, q, k_pad, false, out, err, s);
+}
+
+cudaError_t tk_launch_quantize_levels(const float* x, size_t rows, size_t n, tk_qparams q, int k_pad, bool fp4,
+                                      int8_t* out, unsigned long long* err, cudaStream_t s) {
   const size_t total = rows * (size_t)(k_pad / 16);
   if (total == 0) return cudaSuccess;
   const bool vec4 = (n % 4 == 0) && ((uintptr_t)x % 16 == 0);
-  k_quantize_s8<<<grid_for(total), kThreads, 0, s>>>(x, rows, n, q, k_pad, (rows + 127) / 128 * 128,
+  (fp4 ? k_quantize_s8<true> : k_quantize_s8<false>)<<<grid_for(total), kThreads, 0, s>>>(x, rows, n, q, k_pad, (rows + 127) / 128 * 128,
                                                     out, err, vec4);
   return cudaGetLastError();
 }

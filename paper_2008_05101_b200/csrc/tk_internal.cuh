@@ -41,8 +41,10 @@ struct tk_layer {
   int32_t* d_zcnt = nullptr;    // [out_c] zero lanes per row incl. padding
   float* d_gain = nullptr;      // [out_c]
   float* d_bias = nullptr;      // [out_c]
-  int8_t* d_w8 = nullptr;       // [n_pad][k_pad] s8 tensor-core operand
+  int8_t* d_w8 = nullptr;       // [k_pad/128][n_pad][128] s8 tensor-core operand
+  int8_t* d_w4 = nullptr;       // [k_pad4/256][n_pad][128 B] FP4 (E2M1) operand
   int n_pad = 0, k_pad = 0;
+  int k_pad4 = 0;               // K rounded up to the 256-level FP4 K block
   // host mirrors (PackedConvLayer::weights / weight_sums)
   uint64_t* h_words = nullptr;
   int32_t* h_wsum = nullptr;
@@ -99,6 +101,11 @@ cudaError_t tk_launch_expand_rows_s8(const uint64_t* rows, size_t row_count,
 cudaError_t tk_launch_quantize_s8(const float* x, size_t rows, size_t n,
                                   tk_qparams q, int k_pad, int8_t* out,
                                   unsigned long long* err, cudaStream_t s);
+// fp4: E2M1 nibbles, [k_pad/256][m_pad][128 B] (k_pad a multiple of 256)
+cudaError_t tk_launch_expand_rows(const uint64_t* rows, size_t row_count, int wpr64, int offset, int k_pad,
+                                  bool fp4, int8_t* out, cudaStream_t s);
+cudaError_t tk_launch_quantize_levels(const float* x, size_t rows, size_t n, tk_qparams q, int k_pad, bool fp4,
+                                      int8_t* out, unsigned long long* err, cudaStream_t s);
 
 // launchers (tk_popc.cu)
 cudaError_t tk_launch_dot_batched(const uint64_t* x, const uint64_t* y,
@@ -121,6 +128,8 @@ cudaError_t tk_launch_gemm_popc(const uint64_t* rows, size_t M, int wpr64,
 
 // launchers (tk_tc.cu)
 bool tk_tc_supported(int M, int N, int k_pad);
+cudaError_t tk_launch_gemm_tc_fmt(const int8_t* a, int M, int k_pad, const tk_layer* L, tk_epilogue e, bool fp4,
+                                  cudaStream_t s);
 cudaError_t tk_launch_gemm_tc(const int8_t* a_s8, int M, int k_pad,
                               const tk_layer* L, tk_epilogue e,
                               cudaStream_t s);

@@ -93,6 +93,21 @@ __device__ __forceinline__ void bulk_store(void* dst, const void* src, uint32_t 
                "r"(bytes)
                : "memory");
 }
+// 2-D tensor store shared::cta -> global (bulk group); out-of-bounds clipped
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(map),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1)
+               : "memory");
+}
+// wait until at most N bulk groups still read their shared-memory source
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+// named barrier `id` over `count` threads (multiple of 32)
+__device__ __forceinline__ void named_bar_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 // generic-proxy shared-memory writes -> visible to the async proxy (TMA, bulk copies)
@@ -311,6 +326,33 @@ __device__ __forceinline__ void mma_commit_elect(uint64_t* bar) {
       "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
       "}\n" ::"r"(smem_u32(bar))
       : "memory");
+}
+// FP4 (E2M1) block-scaled MMA, K = 64 per instruction (32 bytes per K-major
+// row), f32 accumulate; sfa / sfb: TMEM addresses of the E8M0 scale factors
+// (all 127 = 2^0 here, so the products are the exact integer levels)
+__device__ __forceinline__ void mma_f4_elect(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                             uint32_t accumulate, uint32_t sfa, uint32_t sfb) {
+  asm volatile(
+      "{\n"
+      ".reg .pred e, p;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(sfa), "r"(sfb));
+}
+// block-scaled instruction descriptor: A/B E2M1 (MXF4 format 1), E8M0 scales, K64
+__host__ __device__ constexpr uint32_t idesc_f4(int M, int N) {
+  return (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | (1u << 23) | ((uint32_t)(M >> 4) << 24);
+}
+// fill NC TMEM columns of this warp's lane quarter with E8M0 unit scales
+template <int NC>
+__device__ __forceinline__ void tmem_fill_unit_scales(uint32_t taddr_quarter) {
+#pragma unroll 4
+  for (int c = 0; c < NC; c += 4)
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %1, %1, %1};" ::"r"(taddr_quarter + c),
+                 "r"(0x7F7F7F7Fu));
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
 // commit that arrives on the mbarrier at the offset of `bar` in every CTA of
 // `mask` (elect.sync inside, like mma_commit_elect)

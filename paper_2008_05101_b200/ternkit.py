@@ -44,6 +44,7 @@ class Backend(IntEnum):
     AUTO = T.TK_BACKEND_AUTO
     POPC = T.TK_BACKEND_POPC
     TC_I8 = T.TK_BACKEND_TC_I8
+    TC_F4 = T.TK_BACKEND_TC_F4
 
 
 @dataclass
@@ -581,40 +582,60 @@ def fully_connected_ternary(x, batch: int, layer: PackedConvLayer,
 # level-operand entry points (tensor-core path without the 2-bit pack step)
 
 
-class LevelOperand:
-    """s8 quantization levels of `rows` rows in the tensor-core operand layout
-    (K-block-major [k_pad/128][m_pad][128], see include/ternkit_b200.h)."""
+# E2M1 nibble of each level -1, 0, 1, 2 (the FP4 operand, include/ternkit_b200.h)
+_E2M1 = {-1: 0xA, 0: 0x0, 1: 0x2, 2: 0x4}
 
-    def __init__(self, data: torch.Tensor, rows: int, k_pad: int):
-        self.data, self.rows, self.k_pad = data, rows, k_pad
+
+class LevelOperand:
+    """Quantization levels of `rows` rows in a tensor-core operand layout.
+
+    fmt "s8": one s8 level per byte, K-block-major [k_pad/128][m_pad][128].
+    fmt "fp4": E2M1 nibbles (even k low), [k_pad/256][m_pad][128 B]."""
+
+    def __init__(self, data: torch.Tensor, rows: int, k_pad: int, fmt: str = "s8"):
+        self.data, self.rows, self.k_pad, self.fmt = data, rows, k_pad, fmt
 
     def dense(self) -> torch.Tensor:
-        """[rows][k_pad] view (a copy), for inspection and tests."""
-        return self.data.permute(1, 0, 2).reshape(-1, self.k_pad)[: self.rows]
+        """[rows][k_pad] s8 levels (a copy), for inspection and tests."""
+        if self.fmt == "s8":
+            return self.data.permute(1, 0, 2).reshape(-1, self.k_pad)[: self.rows]
+        b = self.data.permute(1, 0, 2).reshape(-1, self.k_pad // 2)[: self.rows].to(torch.int32)
+        nib = torch.stack([b & 0xF, b >> 4], dim=-1).reshape(b.shape[0], -1)
+        lut = torch.full((16,), 127, dtype=torch.int8, device=b.device)
+        for lv, code in _E2M1.items():
+            lut[code] = lv
+        return lut[nib.long()]
 
 
-def quantize_levels(x, t: QuantThresholds, mode: QuantMode, k_pad: int) -> LevelOperand:
-    """f32 [rows][n] -> s8 quantization levels (zero padded to k_pad)."""
+def quantize_levels(x, t: QuantThresholds, mode: QuantMode, k_pad: int, fmt: str = "s8") -> LevelOperand:
+    """f32 [rows][n] -> quantization levels (zero padded to k_pad) in `fmt`."""
     xd = _dev(x, torch.float32)
     rows, n = xd.shape
     m_pad = (rows + 127) // 128 * 128
-    out = torch.zeros((k_pad // 128, m_pad, 128), dtype=torch.int8, device="cuda")
-    check(T.lib().tk_quantize_levels(context(), _p(xd), rows, n, t.alpha1, t.alpha2, int(mode), k_pad,
-                                     _p(out), _stream()), "quantize_levels")
-    return LevelOperand(out, rows, k_pad)
+    if fmt == "s8":
+        out = torch.zeros((k_pad // 128, m_pad, 128), dtype=torch.int8, device="cuda")
+        fn = T.lib().tk_quantize_levels
+    elif fmt == "fp4":
+        out = torch.zeros((k_pad // 256, m_pad, 128), dtype=torch.uint8, device="cuda")
+        fn = T.lib().tk_quantize_levels_fp4
+    else:
+        raise ValueError(f"unknown level format {fmt!r}")
+    check(fn(context(), _p(xd), rows, n, t.alpha1, t.alpha2, int(mode), k_pad, _p(out), _stream()),
+          "quantize_levels")
+    return LevelOperand(out, rows, k_pad, fmt)
 
 
 def gemm_levels(a: LevelOperand, layer: PackedConvLayer, fused: bool = False,
                 out: torch.Tensor | None = None) -> torch.Tensor:
-    """Ternary GEMM on s8 level operands: int32 accumulators, or (fused=True)
-    f32 rows after the folded-BN epilogue."""
+    """Ternary GEMM on level operands (s8: kind::i8, fp4: kind::mxf4): int32
+    accumulators, or (fused=True) f32 rows after the folded-BN epilogue."""
     m = a.rows
     if out is None:
         out = torch.empty((m, layer.geom.out_c), dtype=torch.float32 if fused else torch.int32, device="cuda")
-    check(T.lib().tk_gemm_levels(context(), layer.handle, _p(a.data), m, 1 if fused else 0, _p(out),
-                                 _stream()), "gemm_levels")
+    fn = T.lib().tk_gemm_levels_fp4 if a.fmt == "fp4" else T.lib().tk_gemm_levels
+    check(fn(context(), layer.handle, _p(a.data), m, 1 if fused else 0, _p(out), _stream()), "gemm_levels")
     return out
 
 
-def layer_k_pad(layer: PackedConvLayer) -> int:
-    return T.lib().tk_layer_k_pad(layer.handle)
+def layer_k_pad(layer: PackedConvLayer, fmt: str = "s8") -> int:
+    return (T.lib().tk_layer_k_pad_fp4 if fmt == "fp4" else T.lib().tk_layer_k_pad)(layer.handle)

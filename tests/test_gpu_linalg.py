@@ -1,6 +1,6 @@
 """GPU parity: im2col_quantize_pack, packed_gemm, conv2d_ternary and
 fully_connected_ternary vs the reference's golden outputs and the C oracle,
-on both pipes (LOP3+POPC and tcgen05 kind::i8).  Integers and packed words
+on every pipe (LOP3+POPC, tcgen05 kind::i8 and kind::mxf4).  Integers and packed words
 bit-exact; float epilogue bit-exact (same FMA shape as the reference build)."""
 import numpy as np
 import pytest
@@ -14,7 +14,7 @@ def u64(t):
 
 
 def backends(tk):
-    return [tk.Backend.POPC, tk.Backend.TC_I8]
+    return [tk.Backend.POPC, tk.Backend.TC_I8, tk.Backend.TC_F4]
 
 
 def _layer(tk, wq, c, oc, k, s, p, ta=(0.5, 0.9), nonneg=True, gain=None, bias=None, out_scale=1.0,
@@ -45,7 +45,7 @@ def test_im2col_kats(tk, golden):
                                 QM.kWeight)
 
 
-@pytest.mark.parametrize("backend", ["POPC", "TC_I8"])
+@pytest.mark.parametrize("backend", ["POPC", "TC_I8", "TC_F4"])
 def test_conv_shapes_golden(tk, golden, backend):
     QT, QM, TS, CG = tk.QuantThresholds, tk.QuantMode, tk.TensorShape, tk.ConvGeometry
     for i, (c, r, k, s, p, b) in enumerate(golden["conv_shapes"]):
@@ -111,7 +111,7 @@ def test_selector_row(tk):
     assert list(out) == want
 
 
-@pytest.mark.parametrize("backend", ["POPC", "TC_I8"])
+@pytest.mark.parametrize("backend", ["POPC", "TC_I8", "TC_F4"])
 def test_conv_properties(tk, oracle, backend):
     """Batch independence (exact), out_scale linearity, geometry grid, zero-input FC
     (R:tests/test_linalg.cpp:267-380)."""
@@ -151,7 +151,7 @@ def test_conv_properties(tk, oracle, backend):
     assert list(y[0]) == [0.5, -0.5, 4.0]
 
 
-@pytest.mark.parametrize("backend", ["POPC", "TC_I8"])
+@pytest.mark.parametrize("backend", ["POPC", "TC_I8", "TC_F4"])
 def test_fc_golden_and_geometry(tk, golden, backend):
     for name in ("fc_small", "fc_mid"):
         bt, cin, cout = map(int, golden[f"{name}_dims"])
@@ -165,7 +165,7 @@ def test_fc_golden_and_geometry(tk, golden, backend):
         tk.fully_connected_ternary(np.zeros(60, np.float32), 3, bad)
 
 
-@pytest.mark.parametrize("backend", ["POPC", "TC_I8"])
+@pytest.mark.parametrize("backend", ["POPC", "TC_I8", "TC_F4"])
 def test_fc_cfg3_full_size(tk, oracle, backend):
     """cfg3: FC 4096x4096, batch 256 -- exact int32 accumulators vs a numpy
     integer matmul of the decoded levels (size-independent exactness), and the
@@ -192,17 +192,20 @@ def test_fc_cfg3_full_size(tk, oracle, backend):
     assert np.array_equal(y[rows].view(np.int32), ref.reshape(xs.shape[0], N).view(np.int32))
 
 
-@pytest.mark.parametrize("rows,k,n", [(256, 4096, 4096), (200, 640, 96), (1, 128, 8), (300, 1280, 260)])
-def test_level_operand_gemm(tk, oracle, rows, k, n):
+@pytest.mark.parametrize("fmt", ["s8", "fp4"])
+@pytest.mark.parametrize("rows,k,n", [(256, 4096, 4096), (200, 640, 96), (1, 128, 8), (300, 1280, 260),
+                                      (128, 40000, 64)])
+def test_level_operand_gemm(tk, oracle, rows, k, n, fmt):
     """quantize_levels -> gemm_levels (the cfg3 kernels on their own): levels
     equal the oracle quantizer, int32 accumulators equal the integer matmul,
-    across split-K cluster sizes (ragged rows / columns included)."""
+    across split-K cluster sizes (ragged rows / columns included; K = 40000
+    forces the split that keeps the s16 partials exact)."""
     rng = np.random.default_rng(rows + k + n)
     wq = rng.integers(-1, 2, (n, k)).astype(np.int8)
     layer = _layer(tk, wq, k, n, 1, 1, 0)
     x = np.abs(rng.standard_normal((rows, k))).astype(np.float32)
     a = tk.quantize_levels(torch.from_numpy(x).cuda(), tk.QuantThresholds(0.5, 0.9), tk.QuantMode.kActivationNonneg,
-                           tk.layer_k_pad(layer))
+                           tk.layer_k_pad(layer, fmt), fmt)
     lv = a.dense().cpu().numpy()[:, :k].astype(np.int64)
     st, words = oracle.quantize_and_pack(x[: min(rows, 8)].reshape(-1), 0.5, 0.9, 1)
     want_lv = oracle.unpack(words, min(rows, 8) * k).reshape(min(rows, 8), k).astype(np.int64) + 1
@@ -217,3 +220,22 @@ def test_level_operand_gemm(tk, oracle, rows, k, n):
     r4 = min(rows, 4)  # fmaf epilogue: the oracle's conv epilogue on the same inputs
     st, yo = oracle.conv2d_ternary(x[:r4], r4, k, 1, 1, wq, n, 1, 1, 0, (0.5, 0.9), True, gain, bias, 1.0)
     assert st == 0 and np.array_equal(y[:r4].view(np.int32), yo.reshape(r4, n).view(np.int32))
+
+
+def test_fp4_symmetric_levels(tk):
+    """kind::mxf4 with -1 levels on both sides (weight-mode activations into a
+    symmetric layer): identical to the s8 path and the integer matmul."""
+    rng = np.random.default_rng(71)
+    rows, k, n = 384, 1000, 200
+    wq = rng.integers(-1, 2, (n, k)).astype(np.int8)
+    layer = _layer(tk, wq, k, n, 1, 1, 0, ta=(0.8, 1.2), nonneg=False)
+    x = torch.from_numpy(rng.standard_normal((rows, k)).astype(np.float32)).cuda()
+    a8 = tk.quantize_levels(x, tk.QuantThresholds(0.8, 1.2), tk.QuantMode.kWeight, tk.layer_k_pad(layer))
+    a4 = tk.quantize_levels(x, tk.QuantThresholds(0.8, 1.2), tk.QuantMode.kWeight, tk.layer_k_pad(layer, "fp4"),
+                            "fp4")
+    lv = a8.dense().cpu().numpy()[:, :k]
+    assert np.array_equal(a4.dense().cpu().numpy()[:, :k], lv)
+    assert not a4.dense().cpu().numpy()[:, k:].any()
+    want = lv.astype(np.int64) @ wq.T.astype(np.int64)
+    assert np.array_equal(tk.gemm_levels(a4, layer).cpu().numpy(), want)
+    assert np.array_equal(tk.gemm_levels(a8, layer).cpu().numpy(), want)

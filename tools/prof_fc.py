@@ -17,10 +17,12 @@ def main():
     wq = rng.integers(-1, 2, (N, C)).astype(np.int8)
     layer = tk.make_packed_conv_layer(wq, tk.ConvGeometry(C, N, 1, 1, 1, 0), tk.QuantThresholds(),
                                       tk.QuantThresholds(0.5, 0.9), True)
-    layer.set_backend(tk.Backend[os.environ.get("BACKEND", "TC_I8")])
+    backend = os.environ.get("BACKEND", "TC_I8")
+    layer.set_backend(tk.Backend[backend])
+    fmt = "fp4" if backend == "TC_F4" else "s8"
     x = torch.from_numpy(np.abs(rng.standard_normal((B, C))).astype(np.float32)).cuda()
     a8 = tk.quantize_levels(x, tk.QuantThresholds(0.5, 0.9), tk.QuantMode.kActivationNonneg,
-                            tk.layer_k_pad(layer))
+                            tk.layer_k_pad(layer, fmt), fmt)
     out = torch.empty((B, N), dtype=torch.int32, device="cuda")
     for _ in range(3):
         tk.gemm_levels(a8, layer, out=out)
@@ -39,7 +41,7 @@ def main():
     e1.record()
     e1.synchronize()
     ms = e0.elapsed_time(e1) / 10
-    print(f"gemm {B}x{N}x{C}: {ms * 1e3:.2f} us/launch (L2-warm, back-to-back) = "
+    print(f"{fmt} gemm {B}x{N}x{C}: {ms * 1e3:.2f} us/launch (L2-warm, back-to-back) = "
           f"{2 * B * N * C / ms / 1e9:.1f} TOPS")
     lv = tk.unpack(tk.PackedTernaryVector(tk.quantize_and_pack_rows(x[:2], tk.QuantThresholds(0.5, 0.9),
                    tk.QuantMode.kActivationNonneg).view(-1), 2 * C)).cpu().numpy().reshape(2, C) + 1
