@@ -632,16 +632,20 @@ __global__ void k_residual_relu(float* __restrict__ z, const float* __restrict__
 // ---------------------------------------------------------------------------
 // stem convolution (float, outside the ternary path): 7x7 / stride 2 / pad 3,
 // 3 -> 64 channels, fp32 FMA accumulation in the fixed order (ci, ky, kx).
-// CTA = one image, kStemRows output rows x the full width; 256 threads =
-// 4 channel groups (16 channels) x 64 pixel groups (7 consecutive columns of
-// one row), 112 accumulators per thread.  Input band and weights in SMEM;
-// per tap 4 x LDS.128 (weights, broadcast) + 7 LDS (inputs) feed 112 FFMA.
+// CTA = one image, kStemRows output rows x the full width; 512 threads =
+// 8 channel groups (8 channels) x 64 pixel groups (7 columns, 16 apart, of
+// one row), 56 accumulators per thread (four warps per scheduler keep the
+// FMA pipe fed; FFMA2 occupies it for two cycles, so it halves issue slots,
+// not pipe time).  Input band and weights in SMEM; per tap 2 x LDS.128
+// (weights, broadcast) + 7 LDS (inputs) feed 56 FMA.
 constexpr int kStemRows = 4, kStemCols = 112, kStemPx = 7;
 constexpr int kStemInRows = 2 * kStemRows + 5, kStemInCols = 2 * kStemCols + 6;
 // the input band is stored as even / odd column planes (stride-2 taps read
-// consecutive words); plane pitch 120 = 8 mod 16 puts the two image rows a
-// warp reads 16 banks apart: conflict-free shared loads
-constexpr int kStemHalf = kStemInCols / 2, kStemPitch = 120;
+// consecutive words); the two output rows a warp computes read input rows
+// 2 apart, i.e. 4 plane pitches: pitch 116 (4 mod 8) puts them 16 banks
+// apart, so the 32 lanes' input loads are conflict-free
+constexpr int kStemHalf = kStemInCols / 2, kStemPitch = 116;
+static_assert(kStemPitch >= kStemHalf && (4 * kStemPitch) % 32 == 16, "stem band pitch");
 
 // Persistent: one CTA per SM loads the weights once and walks (image, row
 // tile) items; the next item's input band streams in with cp.async (zero
@@ -660,21 +664,26 @@ __device__ __forceinline__ void stem_fill_band(float* band, const float* __restr
   asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
-__global__ void __launch_bounds__(256, 1)
+// CPT channels per thread (8: 512 threads, 16: 256 threads); PAIR: packed
+// fp32x2 FMA (FFMA2) on channel pairs, else scalar FFMA -- every lane of
+// either form is one round-to-nearest fp32 FMA in the same (ci, ky, kx) order
+template <int CPT, bool PAIR>
+__global__ void __launch_bounds__(64 * 64 / CPT, 1)
 k_stem_conv(const float* __restrict__ img, const float* __restrict__ wgt, int N, int H, int W, int Ho, int Wo,
             float* __restrict__ out) {
+  constexpr int kThr = 64 * 64 / CPT;
   extern __shared__ __align__(16) float s_stem[];
   float* s_w = s_stem;                                     // [tap][cout]
   constexpr int kBand = 3 * kStemInRows * 2 * kStemPitch;  // [ci][row][parity][kStemPitch]
   float* s_band[2] = {s_stem + 147 * 64, s_stem + 147 * 64 + kBand};
-  for (int i = threadIdx.x; i < 147 * 64; i += 256) {
+  for (int i = threadIdx.x; i < 147 * 64; i += kThr) {
     const int co = i / 147, tap = i - co * 147;  // weights [cout][ci][ky][kx]
     s_w[tap * 64 + co] = __ldg(wgt + i);
   }
   const int tiles = (Ho + kStemRows - 1) / kStemRows, n_items = N * tiles;
   int item = blockIdx.x;
   if (item < n_items) stem_fill_band(s_band[0], img, item / tiles, (item % tiles) * kStemRows, H, W);
-  const int cg = threadIdx.x >> 6;      // channel group of 16 (warp-uniform)
+  const int cg = threadIdx.x >> 6;      // channel group of CPT (warp-uniform)
   const int pg = threadIdx.x & 63;
   const int row = pg >> 4, c0 = pg & 15;  // output columns c0, c0+16, ..., c0+96
   for (int buf = 0; item < n_items; item += gridDim.x, buf ^= 1) {
@@ -687,14 +696,11 @@ k_stem_conv(const float* __restrict__ img, const float* __restrict__ wgt, int N,
     }
     __syncthreads();
     const float* s_in = s_band[buf];
-    // packed fp32x2 FMA (FFMA2): channel pairs (c, c+1) per instruction, the
-    // input value broadcast to both halves -- each half is an ordinary
-    // round-to-nearest fp32 FMA, so the results are those of __fmaf_rn
-    unsigned long long acc[8][kStemPx];
+    float acc[CPT][kStemPx];
 #pragma unroll
-    for (int c = 0; c < 8; ++c)
+    for (int c = 0; c < CPT; ++c)
 #pragma unroll
-      for (int j = 0; j < kStemPx; ++j) acc[c][j] = 0ull;
+      for (int j = 0; j < kStemPx; ++j) acc[c][j] = 0.0f;
 #pragma unroll 1
     for (int ci = 0; ci < 3; ++ci)
 #pragma unroll
@@ -702,44 +708,46 @@ k_stem_conv(const float* __restrict__ img, const float* __restrict__ wgt, int N,
         const float* in_row = s_in + (ci * kStemInRows + 2 * row + ky) * 2 * kStemPitch;
 #pragma unroll
         for (int kx = 0; kx < 7; ++kx) {
-          const ulonglong2* w4 =
-              reinterpret_cast<const ulonglong2*>(s_w + ((ci * 7 + ky) * 7 + kx) * 64 + cg * 16);
-          unsigned long long wv[8];
+          const float4* w4 = reinterpret_cast<const float4*>(s_w + ((ci * 7 + ky) * 7 + kx) * 64 + cg * CPT);
+          float wv[CPT];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const ulonglong2 t = w4[q];
-            wv[2 * q] = t.x;
-            wv[2 * q + 1] = t.y;
+          for (int q = 0; q < CPT / 4; ++q) {
+            const float4 t = w4[q];
+            wv[4 * q] = t.x; wv[4 * q + 1] = t.y; wv[4 * q + 2] = t.z; wv[4 * q + 3] = t.w;
           }
           // input column 2*oc + kx (band coordinates) = plane kx&1, word oc + kx/2
           const float* pl = in_row + (kx & 1) * kStemPitch + (kx >> 1) + c0;
-          unsigned long long xv[kStemPx];
+          float xv[kStemPx];
 #pragma unroll
-          for (int j = 0; j < kStemPx; ++j) {
-            const float x = pl[16 * j];
-            asm("mov.b64 %0, {%1, %1};" : "=l"(xv[j]) : "f"(x));
+          for (int j = 0; j < kStemPx; ++j) xv[j] = pl[16 * j];
+          if constexpr (PAIR) {
+#pragma unroll
+            for (int c = 0; c < CPT; c += 2)
+#pragma unroll
+              for (int j = 0; j < kStemPx; ++j) {
+                unsigned long long a, w, x;
+                asm("mov.b64 %0, {%1, %2};" : "=l"(a) : "f"(acc[c][j]), "f"(acc[c + 1][j]));
+                asm("mov.b64 %0, {%1, %2};" : "=l"(w) : "f"(wv[c]), "f"(wv[c + 1]));
+                asm("mov.b64 %0, {%1, %1};" : "=l"(x) : "f"(xv[j]));
+                asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(a) : "l"(w), "l"(x));
+                asm("mov.b64 {%0, %1}, %2;" : "=f"(acc[c][j]), "=f"(acc[c + 1][j]) : "l"(a));
+              }
+          } else {
+#pragma unroll
+            for (int c = 0; c < CPT; ++c)
+#pragma unroll
+              for (int j = 0; j < kStemPx; ++j) acc[c][j] = __fmaf_rn(wv[c], xv[j], acc[c][j]);
           }
-#pragma unroll
-          for (int c = 0; c < 8; ++c)
-#pragma unroll
-            for (int j = 0; j < kStemPx; ++j)
-              asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc[c][j]) : "l"(wv[c]), "l"(xv[j]));
         }
       }
     const int n = item / tiles, oy = (item % tiles) * kStemRows + row;
     if (oy < Ho) {
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        float* o0 = out + ((size_t)(n * 64 + cg * 16 + 2 * c) * Ho + oy) * Wo;
-        float* o1 = o0 + (size_t)Ho * Wo;
+      for (int c = 0; c < CPT; ++c) {
+        float* o = out + ((size_t)(n * 64 + cg * CPT + c) * Ho + oy) * Wo;
 #pragma unroll
         for (int j = 0; j < kStemPx; ++j)
-          if (c0 + 16 * j < Wo) {
-            float lo, hi;
-            asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(acc[c][j]));
-            o0[c0 + 16 * j] = lo;
-            o1[c0 + 16 * j] = hi;
-          }
+          if (c0 + 16 * j < Wo) o[c0 + 16 * j] = acc[c][j];
       }
     }
     __syncthreads();  // everyone is done with this band before it is refilled
@@ -772,6 +780,43 @@ __global__ void k_affine_relu_maxpool(const float* __restrict__ x, int C, int H,
       }
     }
     out[i] = m;
+  }
+}
+
+// the same with 4 consecutive outputs per thread (W = 2 * Wo, Wo % 4 == 0):
+// per input row two float4 loads + one scalar replace 12 scalar loads, and
+// the outputs go out as one float4
+__global__ void k_affine_relu_maxpool4(const float* __restrict__ x, int C, int H, int W, int Ho, int Wo,
+                                       const float* __restrict__ gain, const float* __restrict__ bias,
+                                       long long total4, float* __restrict__ out) {
+  const int q = Wo / 4;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total4;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int ox = (int)(i % q) * 4;
+    const long long r = i / q;
+    const int oy = (int)(r % Ho);
+    const long long nc = r / Ho;
+    const int c = (int)(nc % C);
+    const float g = __ldg(gain + c), b = __ldg(bias + c);
+    const float* src = x + nc * H * W;
+    float m[4] = {0.0f, 0.0f, 0.0f, 0.0f};  // relu output >= 0: 0 is the identity of the max
+#pragma unroll
+    for (int dy = -1; dy <= 1; ++dy) {
+      const int y = 2 * oy + dy;
+      if (y < 0 || y >= H) continue;
+      const float* row = src + (long long)y * W + 2 * ox;
+      const float4 a = __ldg(reinterpret_cast<const float4*>(row));
+      const float4 bb = __ldg(reinterpret_cast<const float4*>(row) + 1);
+      // columns 2ox-1 .. 2ox+7 (the left one absent at the image border)
+      const float v[9] = {ox > 0 ? __fmaf_rn(g, __ldg(row - 1), b) : 0.0f,
+                          __fmaf_rn(g, a.x, b),  __fmaf_rn(g, a.y, b),  __fmaf_rn(g, a.z, b),
+                          __fmaf_rn(g, a.w, b),  __fmaf_rn(g, bb.x, b), __fmaf_rn(g, bb.y, b),
+                          __fmaf_rn(g, bb.z, b), __fmaf_rn(g, bb.w, b)};
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        m[k] = fmaxf(m[k], fmaxf(fmaxf(v[2 * k], v[2 * k + 1]), v[2 * k + 2]));
+    }
+    reinterpret_cast<float4*>(out)[i] = make_float4(m[0], m[1], m[2], m[3]);
   }
 }
 
@@ -1408,6 +1453,12 @@ int tk_affine_relu_maxpool(tk_context* ctx, const float* x, int n, int c, int h,
   const int ho = (h + 1) / 2, wo = (w + 1) / 2;
   const long long total = (long long)n * c * ho * wo;
   if (total == 0) return TK_OK;
+  if (w == 2 * wo && wo % 4 == 0 && h == 2 * ho && (uintptr_t)x % 16 == 0 && (uintptr_t)out % 16 == 0) {
+    const long long total4 = total / 4;
+    const unsigned grid = (unsigned)std::min<long long>((total4 + 255) / 256, 148ll * 32);
+    k_affine_relu_maxpool4<<<grid, 256, 0, (cudaStream_t)stream>>>(x, c, h, w, ho, wo, gain, bias, total4, out);
+    return cudaGetLastError() == cudaSuccess ? TK_OK : TK_ERR_CUDA;
+  }
   const unsigned grid = (unsigned)std::min<long long>((total + 255) / 256, 148ll * 64);
   k_affine_relu_maxpool<<<grid, 256, 0, (cudaStream_t)stream>>>(x, c, h, w, ho, wo, gain, bias, total, out);
   return cudaGetLastError() == cudaSuccess ? TK_OK : TK_ERR_CUDA;
@@ -1420,14 +1471,26 @@ int tk_stem_conv7x7s2(tk_context* ctx, const float* images, int n, int h, int w,
   if (wo > kStemCols || (w + 6) > kStemInCols) return TK_ERR_UNSUPPORTED;  // one CTA spans the width
   if (n == 0) return TK_OK;
   const int smem = (147 * 64 + 2 * 3 * kStemInRows * 2 * kStemPitch) * 4;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_stem_conv, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
+  // variant (A/B knob TK_STEM_VARIANT): 1 = 8 channels x FFMA2 (512 threads,
+  // the default: fastest measured), 0 = 16 x FFMA2 (256), 2 = 16 x FFMA
+  // (256), 3 = 8 x FFMA (512)
+  static const int variant = getenv("TK_STEM_VARIANT") ? atoi(getenv("TK_STEM_VARIANT")) : 1;
+  auto go = [&](auto kern, int threads) {
+    static bool attr[4] = {false, false, false, false};
+    if (!attr[variant & 3]) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      attr[variant & 3] = true;
+    }
+    const int items = n * ((ho + kStemRows - 1) / kStemRows);
+    kern<<<std::min(items, ctx->num_sms), threads, smem, (cudaStream_t)stream>>>(images, weights, n, h, w, ho, wo,
+                                                                                 out);
+  };
+  switch (variant & 3) {
+    case 1: go(k_stem_conv<8, true>, 512); break;
+    case 2: go(k_stem_conv<16, false>, 256); break;
+    case 3: go(k_stem_conv<8, false>, 512); break;
+    default: go(k_stem_conv<16, true>, 256); break;
   }
-  const int items = n * ((ho + kStemRows - 1) / kStemRows);
-  k_stem_conv<<<std::min(items, ctx->num_sms), 256, smem, (cudaStream_t)stream>>>(images, weights, n, h, w, ho, wo,
-                                                                                  out);
   return cudaGetLastError() == cudaSuccess ? TK_OK : TK_ERR_CUDA;
 }
 

@@ -190,7 +190,7 @@ class TernaryResNet:
         self.head_w = (torch.randn(classes, c, generator=g) / math.sqrt(c)).cuda()
         self.head_b = torch.zeros(classes).cuda()
 
-    def stem(self, images: torch.Tensor) -> torch.Tensor:
+    def stem(self, images: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         """fp32 7x7/2 conv (tk_stem_conv7x7s2: SIMT FMA, no tensor-core
         rounding), then one fused pass of folded BN (fmaf), ReLU and 3x3/2
         max-pool (tk_affine_relu_maxpool)."""
@@ -205,7 +205,8 @@ class TernaryResNet:
                                             self.stem_w.data_ptr(), y.data_ptr(), tk._stream()),
                   "tk_stem_conv7x7s2")
         n, c, h, w = y.shape
-        out = torch.empty((n, c, (h + 1) // 2, (w + 1) // 2), dtype=torch.float32, device="cuda")
+        if out is None:
+            out = torch.empty((n, c, (h + 1) // 2, (w + 1) // 2), dtype=torch.float32, device="cuda")
         check(T.lib().tk_affine_relu_maxpool(tk.context(), y.data_ptr(), n, c, h, w, self.stem_gain.data_ptr(),
                                              self.stem_bias.data_ptr(), out.data_ptr(), tk._stream()),
               "tk_affine_relu_maxpool")
@@ -221,17 +222,27 @@ class TernaryResNet:
 
 
 class PipelinedResNet:
-    """End-to-end inference from host images with the host->device copy of
-    image chunk i+1 (copy stream) overlapping stem + body + head of chunk i
-    (compute stream).  Shares the stem/head parameters and block spec of
-    `net`; the body runs on `chunk`-image slices (its own TernaryBody)."""
+    """End-to-end inference from host images.  The batch is uploaded in
+    `chunks` slices on a copy stream; each slice's stem runs (compute stream)
+    as soon as it has landed, and the ternary body runs on groups of
+    consecutive slices (`groups`: slices per body launch sequence, default
+    one group per slice) once their stems are done -- so the body of an
+    early group overlaps the upload of later slices, and only the last
+    group's stem + body follow the final copy.  Shares the stem/head
+    parameters and block spec of `net`."""
 
-    def __init__(self, net: TernaryResNet, batch: int, chunks: int = 4):
+    def __init__(self, net: TernaryResNet, batch: int, chunks: int = 4, groups: list[int] | None = None):
         assert batch % chunks == 0
-        self.net, self.batch, self.chunks, self.cb = net, batch, chunks, batch // chunks
-        self.body = TernaryBody(net.blocks, self.cb, 64, 56, 56)
+        groups = list(groups) if groups else [1] * chunks
+        assert sum(groups) == chunks and all(g > 0 for g in groups)
+        self.net, self.batch, self.chunks, self.cb, self.groups = net, batch, chunks, batch // chunks, groups
+        sizes = sorted(set(groups))
+        self.bodies = {g: TernaryBody(net.blocks, g * self.cb, 64, 56, 56) for g in sizes}
+        self.body = self.bodies[sizes[-1]]
         self.copy_stream = torch.cuda.Stream()
         self.img = [torch.empty((self.cb, 3, 224, 224), device="cuda") for _ in range(chunks)]
+        # stem outputs of a group, contiguous so the group's body reads one tensor
+        self.xg = [torch.empty((g * self.cb, 64, 56, 56), device="cuda") for g in groups]
         self.ev_copied = [torch.cuda.Event() for _ in range(chunks)]
         self.ev_consumed = [torch.cuda.Event() for _ in range(chunks)]
         self.pooled = torch.empty((batch, self.body.out_shape[0]), device="cuda")
@@ -241,17 +252,21 @@ class PipelinedResNet:
     def forward(self, images_host: torch.Tensor) -> torch.Tensor:
         cs = torch.cuda.current_stream()
         self.copy_stream.wait_stream(cs)  # previous users of the outputs are ordered
-        for i in range(self.chunks):
-            sl = slice(i * self.cb, (i + 1) * self.cb)
-            with torch.cuda.stream(self.copy_stream):
+        with torch.cuda.stream(self.copy_stream):
+            for i in range(self.chunks):
                 if not self._first:  # the previous step's stem has read this buffer
                     self.copy_stream.wait_event(self.ev_consumed[i])
-                self.img[i].copy_(images_host[sl], non_blocking=True)
+                self.img[i].copy_(images_host[i * self.cb:(i + 1) * self.cb], non_blocking=True)
                 self.ev_copied[i].record(self.copy_stream)
-            cs.wait_event(self.ev_copied[i])
-            x = self.net.stem(self.img[i])
-            self.ev_consumed[i].record(cs)
-            self.body.forward(x, pooled=self.pooled[sl], check_errors=False)
+        i = 0
+        for gi, g in enumerate(self.groups):
+            for k in range(g):
+                cs.wait_event(self.ev_copied[i])
+                self.net.stem(self.img[i], out=self.xg[gi][k * self.cb:(k + 1) * self.cb])
+                self.ev_consumed[i].record(cs)
+                i += 1
+            lo = (i - g) * self.cb
+            self.bodies[g].forward(self.xg[gi], pooled=self.pooled[lo:lo + g * self.cb], check_errors=False)
         self._first = False
         return self.net.head(self.pooled, out=self.logits)
 
@@ -287,8 +302,20 @@ class ResNetWorkload:
         self.pooled = torch.empty((batch, self.net.body.out_shape[0]), device="cuda")
         self.logits_host = torch.empty((global_batch if rank == 0 else 0, 1000)).pin_memory()
         # e2e: chunked so the image upload overlaps the compute of earlier chunks
-        chunks = int(os.environ.get("TK_E2E_CHUNKS", 4 if batch % 4 == 0 and batch >= 64 else 1))
-        self.pipe = PipelinedResNet(self.net, batch, chunks)
+        # (measured, tools/gpu_e2e.sh, R18 b256: 8 slices with the body on two
+        # halves 3.96 ms; 4 slices, body per slice 4.24 ms)
+        if batch % 8 == 0 and batch >= 128:
+            chunks, groups = 8, [4, 4]
+        elif batch % 4 == 0 and batch >= 64:
+            chunks, groups = 4, [2, 2]
+        else:
+            chunks, groups = 1, [1]
+        chunks = int(os.environ.get("TK_E2E_CHUNKS", chunks))
+        if os.environ.get("TK_E2E_GROUPS"):
+            groups = [int(g) for g in os.environ["TK_E2E_GROUPS"].split(",")]
+        elif sum(groups) != chunks:
+            groups = None
+        self.pipe = PipelinedResNet(self.net, batch, chunks, groups)
         self.sharded = ShardedForward(lambda _x: self.pipe.forward(self.images_host), global_batch, 1000, rank,
                                       world)
         self.macs_per_img = body_macs(self.net.blocks)

@@ -129,6 +129,11 @@ def test_pipelined_e2e_matches_serial_chunks(tk):
     torch.cuda.synchronize()
     assert torch.equal(pipe.pooled, pooled)  # stem + ternary body, chunk by chunk: bit-exact
     assert torch.equal(got, net.head(pooled))  # (one head GEMM over the whole batch, as the pipeline does)
+    # body launched on groups of 2 + 1 + 1 uploaded slices: the same bits
+    pipe_g = PipelinedResNet(net, 16, chunks=4, groups=[2, 1, 1])
+    got_g = pipe_g.forward(imgs).clone()
+    torch.cuda.synchronize()
+    assert torch.equal(pipe_g.pooled, pooled) and torch.equal(got_g, got)
     # fused affine + ReLU + max-pool vs torch (fmaf vs mul+add: within 1 ulp-ish)
     y = torch.nn.functional.conv2d(imgs[:2].cuda(), net.stem_w, stride=2, padding=3)
     ref = torch.nn.functional.max_pool2d(torch.relu(torch.addcmul(net.stem_bias.view(1, -1, 1, 1), y,
