@@ -71,6 +71,7 @@ __global__ void k_im2col(const float* __restrict__ x, int n, int c, int h,
                          int w, int kh, int kw, int stride, int pad, int oh,
                          int ow, int K, int w32pr, tk_qparams q,
                          uint32_t* __restrict__ out, unsigned long long* err) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // (expand waits for this grid)
   const size_t rows = (size_t)n * oh * ow;
   const size_t total = rows * (size_t)w32pr;
   for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total;
@@ -160,6 +161,10 @@ template <bool F4>
 __global__ void k_expand_rows_s8(const uint32_t* __restrict__ rows,
                                  size_t row_count, int w32pr, int offset,
                                  int k_pad, size_t m_pad, int8_t* __restrict__ out) {
+  // launched as a dependent of the row producer (im2col): wait for its rows;
+  // the GEMM after this kernel may launch right away
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int chunks = k_pad / 16;
   const uint32_t tbl = offset ? 0x02010100u : 0x010000FFu;
   // code -> E2M1 nibble (offset: levels 0,1,1,2; symmetric: -1,0,0,1)
@@ -202,6 +207,8 @@ __global__ void k_quantize_s8(const float* __restrict__ x, size_t rows,
                               size_t n, tk_qparams q, int k_pad, size_t m_pad,
                               int8_t* __restrict__ out,
                               unsigned long long* err, bool vec4) {
+  // the consuming GEMM may launch now (it waits for this grid before reading)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int chunks = k_pad / 16;
   const size_t total = rows * (size_t)chunks;
   const int bias = q.nonneg ? 0 : -1;
@@ -319,9 +326,24 @@ cudaError_t tk_launch_expand_rows(const uint64_t* rows, size_t row_count, int wp
                                   bool fp4, int8_t* out, cudaStream_t s) {
   const size_t total = row_count * (size_t)(k_pad / 16);
   if (total == 0) return cudaSuccess;
-  (fp4 ? k_expand_rows_s8<true> : k_expand_rows_s8<false>)<<<grid_for(total), kThreads, 0, s>>>(
-      reinterpret_cast<const uint32_t*>(rows), row_count, 2 * wpr64, offset,
-      k_pad, (row_count + 127) / 128 * 128, out);
+  // programmatic dependent launch: the kernel waits for its predecessor
+  // (griddepcontrol.wait) before touching memory, so only the launch overlaps
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid_for(total));
+  cfg.blockDim = dim3(kThreads);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  const uint32_t* r32 = reinterpret_cast<const uint32_t*>(rows);
+  const size_t m_pad = (row_count + 127) / 128 * 128;
+  const int w32pr = 2 * wpr64;
+  cudaError_t e = fp4 ? cudaLaunchKernelEx(&cfg, k_expand_rows_s8<true>, r32, row_count, w32pr, offset, k_pad, m_pad, out)
+                      : cudaLaunchKernelEx(&cfg, k_expand_rows_s8<false>, r32, row_count, w32pr, offset, k_pad, m_pad,
+                                           out);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 

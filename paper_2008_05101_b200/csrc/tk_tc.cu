@@ -16,9 +16,12 @@
 // (integer sums: exact in any order), applies the epilogue and writes
 // coalesced rows.
 //
-// CTA = 6 warps: warp 0 TMA producer, warp 1 TMEM owner + MMA issuer,
-// warps 2-5 move the accumulator TMEM -> shared memory (TMEM lane quarter =
-// warp % 4); all 6 warps run the cluster reduction + epilogue.
+// CTA = 10 warps: warp 0 TMA producer, warp 1 TMEM owner + MMA issuer,
+// warps 2-9 the epilogue (two per TMEM lane quarter, warp % 4); all warps
+// run the cluster reduction.  Launched with programmatic dependent launch:
+// the prologue and the first weight (B) stages overlap the producing kernel
+// (quantize / expand), A loads and output stores wait for it
+// (griddepcontrol.wait).
 #include <cuda.h>
 
 #include <algorithm>
@@ -151,6 +154,15 @@ k_gemm_tc_i8(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
 
   if (warp == 0) {
     // ---- TMA producer (whole warp waits, lane 0 issues) ----
+    // weights do not depend on the previous kernel: the first stages' B
+    // boxes go out before griddepcontrol.wait, the A boxes after it
+    const int npre = (dbg & 8) ? 0 : min(kStages, kb1 - kb0);
+    if (lane == 0)
+      for (int i = 0; i < npre; ++i) {
+        sm100::mbar_arrive_expect_tx(&full[i], TcSmem<BN>::kStage);
+        sm100::tma_load_2d(sB + i * TcSmem<BN>::kB, &tmB, &full[i], 0, (kb0 + i) * n_pad + n0);
+      }
+    sm100::pdl_wait();
     int s = 0, round = 0;
     for (int kb = kb0; kb < kb1; ++kb) {
       if (round) sm100::mbar_wait(&empty[s], (round - 1) & 1);
@@ -158,7 +170,10 @@ k_gemm_tc_i8(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
         if (dbg & 8) {  // profiling: no operand traffic
           sm100::mbar_arrive(&full[s]);
         } else {
-          sm100::mbar_arrive_expect_tx(&full[s], TcSmem<BN>::kStage);
+          if (kb - kb0 >= npre) {
+            sm100::mbar_arrive_expect_tx(&full[s], TcSmem<BN>::kStage);
+            sm100::tma_load_2d(sB + s * TcSmem<BN>::kB, &tmB, &full[s], 0, kb * n_pad + n0);
+          }
           // K-block-major operands: each box is one contiguous 16 / BN*128 byte block
           if (mcx > 1) {
             const int part = BM / mcx;
@@ -167,7 +182,6 @@ k_gemm_tc_i8(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
           } else {
             sm100::tma_load_2d(sA + s * TcSmem<BN>::kA, &tmA, &full[s], 0, kb * m_pad + m0);
           }
-          sm100::tma_load_2d(sB + s * TcSmem<BN>::kB, &tmB, &full[s], 0, kb * n_pad + n0);
         }
       }
       __syncwarp();
@@ -209,6 +223,7 @@ k_gemm_tc_i8(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
     if (warp >= 2 && !(dbg & 2)) {
       const int q = warp & 3, half = (warp - 2) >> 2;
       uint8_t* buf = smem + (warp - 2) * 8192;  // the operand ring is idle once tmem_full fired
+      sm100::pdl_wait();  // (outputs may still be read by the previous kernel)
       sm100::mbar_wait(tmem_full, 0);
       sm100::tc_fence_after();
       const bool f32 = e.mode != TK_EPI_I32;
@@ -283,6 +298,7 @@ k_gemm_tc_i8(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
   constexpr int C8 = BN / 8;  // 16-byte chunks (8 x s16) per row
   auto swz = [](int row, int c) { return (c & ~7) | ((c ^ row) & 7); };
   uint4* recv = reinterpret_cast<uint4*>(own);  // [S][rows_s][C8]
+  if (warp >= 1) sm100::pdl_wait();  // (warp 0 waited before its A loads)
   if (warp >= 2) sm100::mbar_wait(tmem_full, 0);
   sm100::tc_fence_before();
   sm100::cluster_sync();
@@ -564,13 +580,17 @@ cudaError_t launch(const int8_t* a, int M, int num_kb, const tk_layer* L, tk_epi
   cfg.blockDim = dim3(kThreads, 1, 1);
   cfg.dynamicSmemBytes = TcSmem<BN>::kBytes;
   cfg.stream = s;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = mcx;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = S;
+  // programmatic dependent launch (TK_GEMM_PDL=0 disables, for A/B)
+  static const int pdl = getenv("TK_GEMM_PDL") ? atoi(getenv("TK_GEMM_PDL")) : 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = pdl;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   static const int dbg0 = getenv("TK_GEMM_DBG") ? atoi(getenv("TK_GEMM_DBG")) : 0;  // profiling knob
   static int launches = 0;
   const int dbg = (dbg0 & 16) ? (dbg0 | ((launches++ & 1) << 8)) : dbg0;  // stamp buffer parity
