@@ -4,7 +4,6 @@
 # dominant kernel (ncu, cold caches as ncu runs them).  Outputs: gpurun_out/prof/
 set -x
 mkdir -p gpurun_out/prof
-python -c "import __graft_entry__ as g; g.build()" > gpurun_out/prof/build.log 2>&1 || exit 1
 for w in resnet18 resnet50 fc dot conv; do
   timeout 900 python bench.py --workload $w --steps 20 --warmup 5 > gpurun_out/prof/bench_$w.json 2> gpurun_out/prof/bench_$w.err
 done
@@ -17,11 +16,17 @@ timeout 900 ncu --metrics $M --clock-control none --csv -k regex:k_conv_tc -c 19
   python tools/prof_net.py > /dev/null 2>&1
 DEPTH=50 B=128 timeout 900 ncu --metrics $M --clock-control none --csv -k regex:k_conv_tc -c 52 --log-file gpurun_out/prof/traffic_resnet50.csv \
   python tools/prof_net.py > /dev/null 2>&1
-timeout 600 ncu --metrics $M --clock-control none --csv -k regex:k_gemm_tc -c 1 --log-file gpurun_out/prof/traffic_fc.csv \
+BACKEND=TC_F4 timeout 600 ncu --metrics $M --clock-control none --csv -k regex:k_gemm_tc -c 1 --log-file gpurun_out/prof/traffic_fc.csv \
   python tools/prof_fc.py > /dev/null 2>&1
 timeout 600 ncu --metrics $M --clock-control none --csv -k regex:k_dot_batched -c 1 --log-file gpurun_out/prof/traffic_dot.csv \
   python bench.py --workload dot --steps 3 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
 # one full-set capture of the top ResNet-18 conv (stage-1 conv with skip + f32 out)
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_conv_tc -s 1 -c 1 \
   -o gpurun_out/prof/full_r18_conv1 python tools/prof_net.py > gpurun_out/prof/full.log 2>&1
+# one full-set capture of the cfg3 FC GEMM (FP4 pipe, bench tile choice)
+BACKEND=TC_F4 timeout 600 ncu --set full --import-source on --clock-control none -k regex:k_gemm_tc -s 2 -c 1 \
+  -o gpurun_out/prof/full_fc_gemm python tools/prof_fc.py > gpurun_out/prof/full_fc.log 2>&1
+# and of the stem convolution (e2e path)
+B=64 timeout 600 ncu --set full --clock-control none -k regex:k_stem_conv -c 1 \
+  -o gpurun_out/prof/full_stem python tools/stem_split.py > gpurun_out/prof/full_stem.log 2>&1
 ls -la gpurun_out/prof
