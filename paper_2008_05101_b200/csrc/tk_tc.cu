@@ -38,7 +38,6 @@ constexpr int BM = 128, BK = 128;
 // warp 0 TMA producer, warp 1 TMEM owner + MMA issuer, warps 2-9 epilogue:
 // two warps per TMEM lane quarter (q = warp % 4), each taking half the columns
 constexpr int kThreads = 320;
-constexpr int kEpiWarps = 8;
 
 template <int BN>
 struct TcSmem {
