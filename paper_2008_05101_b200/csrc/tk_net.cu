@@ -85,6 +85,14 @@ struct ConvK {
   int N;
   const float* skip;  // NCHW
   float* fout;        // NCHW
+  // exact s16 residual of a downsample conv: that conv stores its integer
+  // accumulators (aout) instead of f32 and the consumer recomputes the folded
+  // BN, fmaf(sk_gain, sk_scale * acc, sk_bias) -- the same f32 bits, half the bytes
+  int16_t* aout;         // NCHW, downsample conv
+  const int16_t* skip16; // NCHW, the block's last conv
+  const float* sk_gain;
+  const float* sk_bias;
+  float sk_scale;
   int o_Hp, o_Wp, o_PH, o_PW;
   int n_q;
   int8_t* q[2];
@@ -153,7 +161,9 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
   // epilogue parameters of all N channels, staged once: int mode
   // [n_q][3][N] (c0, c1, sign), float mode [2][N] (gain, bias)
   uint32_t* eparam = reinterpret_cast<uint32_t*>(wreg + (size_t)wblocks * p.WB);
-  const int ewords = p.ithr ? (p.ithr16 ? p.n_q * p.N : p.n_q * 3 * p.N) : 2 * p.N;
+  // epilogue parameters: integer thresholds, or gain / bias (+ the residual's
+  // gain / bias when it arrives as s16 accumulators)
+  const int ewords = p.ithr ? (p.ithr16 ? p.n_q * p.N : p.n_q * 3 * p.N) : (p.skip16 ? 4 : 2) * p.N;
   uint64_t* bars = reinterpret_cast<uint64_t*>(eparam + ((ewords + 1) & ~1));
   uint64_t* h_full = bars;
   uint64_t* h_empty = h_full + p.hs;
@@ -349,7 +359,10 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
     const long long oplane = (long long)p.Ho * p.Wo;
     for (int i = et; i < ewords; i += kEpiThreads)
       eparam[i] = p.ithr ? (uint32_t)__ldg(p.ithr + i)
-                         : __float_as_uint(__ldg((i < p.N ? p.gain : p.bias - p.N) + i));
+                         : __float_as_uint(__ldg(i < p.N       ? p.gain + i
+                                                 : i < 2 * p.N ? p.bias + (i - p.N)
+                                                 : i < 3 * p.N ? p.sk_gain + (i - 2 * p.N)
+                                                               : p.sk_bias + (i - 3 * p.N)));
     epi_bar<kEpiThreads>();
     sm100::pdl_wait();  // skip inputs / outputs of the neighbouring layers
     const uint32_t* ep = eparam;
@@ -385,14 +398,20 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
       // skip values are independent of the accumulator: the first chunk's
       // loads are issued before waiting for the MMAs, each later chunk's
       // while the previous one is finished (HBM latency off the critical path)
-      const bool pre = p.skip && valid && !(p.dbg & (4 | 512));
+      const bool pre = (p.skip || p.skip16) && valid && !(p.dbg & (4 | 512));
       const float* skp = p.skip + fbase + (long long)(nt * BN) * oplane;
+      const int16_t* skp16 = p.skip16 + fbase + (long long)(nt * BN) * oplane;
       const uint32_t ostride = (uint32_t)oplane;  // CH channel planes < 2^31 elements
-      float sk[CH];
+      float sk[CH];  // f32 skip, or the s16 residual accumulator as a float (exact)
       if (pre) {
         uint32_t off = 0;
+        if (p.skip16) {
 #pragma unroll
-        for (int j = 0; j < CH; ++j, off += ostride) sk[j] = __ldg(skp + off);
+          for (int j = 0; j < CH; ++j, off += ostride) sk[j] = (float)__ldg(skp16 + off);
+        } else {
+#pragma unroll
+          for (int j = 0; j < CH; ++j, off += ostride) sk[j] = __ldg(skp + off);
+        }
       }
       if (p.dbg & 1024)
         sm100::mbar_wait(&a_full[acc], (it / kAcc) & 1);
@@ -462,6 +481,13 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
           continue;
         }
         if constexpr (MT >= 2) continue;  // MT > 1 kernels: integer epilogue only (host-checked)
+        if (p.aout) {  // downsample: exact s16 accumulators (|acc| <= 2K < 2^15, host-checked)
+          int16_t* ob = p.aout + fbase + (long long)n0 * oplane;
+          uint32_t off = 0;
+#pragma unroll
+          for (int j = 0; j < CH; ++j, off += ostride) ob[off] = (int16_t)(int32_t)r[j];
+          continue;
+        }
         const float4* eg = reinterpret_cast<const float4*>(ep + n0);
         const int n4 = p.N / 4;
         float v[CH];
@@ -485,13 +511,32 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
           }
         }
         if (pre) {  // NCHW: lanes = consecutive positions -> coalesced per channel
+          if (p.skip16) {
+            // the downsample conv's own epilogue, R:linalg.hpp:322-323 (fmul(1, x) == x)
+            const float4* sg = reinterpret_cast<const float4*>(ep + 2 * p.N + n0);
 #pragma unroll
-          for (int j = 0; j < CH; ++j) v[j] += sk[j];
+            for (int j = 0; j < CH / 4; ++j) {
+              const float4 g = sg[j], bb = sg[n4 + j];
+              const float gs[4] = {g.x, g.y, g.z, g.w}, bs[4] = {bb.x, bb.y, bb.z, bb.w};
+#pragma unroll
+              for (int i = 0; i < 4; ++i)
+                v[4 * j + i] += __fmaf_rn(gs[i], __fmul_rn(p.sk_scale, sk[4 * j + i]), bs[i]);
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < CH; ++j) v[j] += sk[j];
+          }
           if (c0 + CH < BN) {
-            const float* sb = skp + (size_t)(c0 + CH) * ostride;
             uint32_t off = 0;
+            if (p.skip16) {
+              const int16_t* sb = skp16 + (size_t)(c0 + CH) * ostride;
 #pragma unroll
-            for (int j = 0; j < CH; ++j, off += ostride) sk[j] = __ldg(sb + off);
+              for (int j = 0; j < CH; ++j, off += ostride) sk[j] = (float)__ldg(sb + off);
+            } else {
+              const float* sb = skp + (size_t)(c0 + CH) * ostride;
+#pragma unroll
+              for (int j = 0; j < CH; ++j, off += ostride) sk[j] = __ldg(sb + off);
+            }
           }
         }
         if (p.relu) {
@@ -899,12 +944,22 @@ struct Conv {
   int skip_f = -1, out_f = -1;  // -2 = the forward's input tensor
   int q_idx[2] = {-1, -1};
   int relu = 0;
+  bool is_down = false;  // the block's downsample (1x1 / stride) conv
   ConvK k{};
   CUtensorMap in_map{}, w_map{};
   int smem = 0;
   int grid = 0;
   int MT = 1;  // 128-row M tiles per work item
 };
+
+
+// the downsample residual travels as exact s16 accumulators when they fit
+// (|acc| <= 2 * in_c * k * k); env TK_NET_F32_RESIDUAL=1 keeps f32 (A/B)
+bool s16_ok(const Conv& cv) { return 2 * cv.d.in_c * cv.d.k * cv.d.k < 32768; }
+bool f32_residual_forced() {
+  static const bool f = getenv("TK_NET_F32_RESIDUAL") && atoi(getenv("TK_NET_F32_RESIDUAL"));
+  return f;
+}
 
 }  // namespace
 
@@ -1125,6 +1180,7 @@ int setup_fused(tk_net* net) {
       dv.d = bd.down;
       dv.in_idx = bin[b].idx_down;
       dv.out_f = want_f32(net, bd.down.out_c, conv_out(H, bd.down), conv_out(W, bd.down));
+      dv.is_down = true;
       sc_f = dv.out_f;
       cvs.push_back(dv);
     }
@@ -1226,6 +1282,23 @@ int setup_fused(tk_net* net) {
       k.o_PH = k.o_Hp / 2; k.o_PW = k.o_Wp / 2;
       k.skip = cv.skip_f >= 0 ? net->f32[cv.skip_f].p : nullptr;  // -2: patched at launch
       k.fout = cv.out_f >= 0 ? net->f32[cv.out_f].p : nullptr;
+      k.aout = nullptr;
+      k.skip16 = nullptr;
+      k.sk_gain = k.sk_bias = nullptr;
+      k.sk_scale = 1.0f;
+      if (!f32_residual_forced() && cv.is_down && s16_ok(cv)) {  // (its f32 tensor holds the s16 values)
+        k.aout = reinterpret_cast<int16_t*>(k.fout);
+        k.fout = nullptr;
+      } else if (!f32_residual_forced() && cv.skip_f >= 0) {
+        for (auto& dv : cvs)
+          if (dv.is_down && dv.out_f == cv.skip_f && s16_ok(dv)) {
+            k.skip16 = reinterpret_cast<const int16_t*>(k.skip);
+            k.skip = nullptr;
+            k.sk_gain = dv.d_gain;
+            k.sk_bias = dv.d_bias;
+            k.sk_scale = dv.d.out_scale;
+          }
+      }
       k.n_q = 0;
       for (int o = 0; o < 2; ++o) {
         if (cv.q_idx[o] < 0) continue;
