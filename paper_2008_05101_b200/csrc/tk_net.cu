@@ -357,15 +357,47 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
     const int grp = (warp - 2) >> 2;
     const int plane = p.PHg * p.PWg;
     const long long oplane = (long long)p.Ho * p.Wo;
-    for (int i = et; i < ewords; i += kEpiThreads)
-      eparam[i] = p.ithr ? (uint32_t)__ldg(p.ithr + i)
-                         : __float_as_uint(__ldg(i < p.N       ? p.gain + i
-                                                 : i < 2 * p.N ? p.bias + (i - p.N)
-                                                 : i < 3 * p.N ? p.sk_gain + (i - 2 * p.N)
-                                                               : p.sk_bias + (i - 3 * p.N)));
+    if constexpr (BN >= 128) {
+      for (int i = et; i < ewords; i += kEpiThreads)
+        eparam[i] = p.ithr ? (uint32_t)__ldg(p.ithr + i)
+                           : __float_as_uint(__ldg(i < p.N       ? p.gain + i
+                                                   : i < 2 * p.N ? p.bias + (i - p.N)
+                                                   : i < 3 * p.N ? p.sk_gain + (i - 2 * p.N)
+                                                                 : p.sk_bias + (i - 3 * p.N)));
+    } else {
+      for (int i = et; i < ewords; i += kEpiThreads)
+        eparam[i] = p.ithr ? (uint32_t)__ldg(p.ithr + i)
+                           : __float_as_uint(__ldg((i < p.N ? p.gain : p.bias - p.N) + i));
+    }
     epi_bar<kEpiThreads>();
     sm100::pdl_wait();  // skip inputs / outputs of the neighbouring layers
     const uint32_t* ep = eparam;
+    const uint32_t ostride = (uint32_t)oplane;  // CH channel planes < 2^31 elements
+    const bool has_skip = (p.skip || (BN >= 128 && p.skip16)) && !(p.dbg & (4 | 512));
+    // element offset of (item's first channel, this thread's position) in the
+    // NCHW skip tensor, or -1 when the position is past the batch / padding
+    auto skip_at = [&](int item) -> long long {
+      const int mi = item / p.n_tiles, nt = item - mi * p.n_tiles;
+      const int qrow = (mi * MT + grp % MT) * 128 + qtr * 32 + lane;
+      const int img = qrow / plane, rem = qrow - img * plane;
+      const int oy = rem / p.PWg, ox = rem - (rem / p.PWg) * p.PWg;
+      if (!(qrow < p.m_total && oy < p.Ho && ox < p.Wo)) return -1;
+      return (long long)img * p.N * oplane + (long long)oy * p.Wo + ox + (long long)(nt * BN) * oplane;
+    };
+    // CH skip values (raw bits: f32, or the sign-extended s16 accumulator) of
+    // one chunk; converted only where they are used, so the loads stay in flight
+    auto load_skip = [&](long long base, uint32_t (&skr)[CH]) {
+      uint32_t off = 0;
+      if (p.skip16) {
+#pragma unroll
+        for (int j = 0; j < CH; ++j, off += ostride) skr[j] = (uint32_t)(int32_t)__ldg(p.skip16 + base + off);
+      } else {
+#pragma unroll
+        for (int j = 0; j < CH; ++j, off += ostride) skr[j] = __float_as_uint(__ldg(p.skip + base + off));
+      }
+    };
+    uint32_t skr[CH];        // skip values of the next chunk to consume
+    bool skr_ready = false;  // skr already holds this item's first chunk (loaded one item ahead)
     int it = 0;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
       // MT == 1: the groups take turns on items; MT > 1: group g takes M tile
@@ -396,22 +428,21 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
       // NCHW index of (img, channel 0, oy, ox) in the f32 skip / output tensors
       const long long fbase = (long long)img * p.N * oplane + (long long)oy * p.Wo + ox;
       // skip values are independent of the accumulator: the first chunk's
-      // loads are issued before waiting for the MMAs, each later chunk's
-      // while the previous one is finished (HBM latency off the critical path)
-      const bool pre = (p.skip || p.skip16) && valid && !(p.dbg & (4 | 512));
-      const float* skp = p.skip + fbase + (long long)(nt * BN) * oplane;
-      const int16_t* skp16 = p.skip16 + fbase + (long long)(nt * BN) * oplane;
-      const uint32_t ostride = (uint32_t)oplane;  // CH channel planes < 2^31 elements
-      float sk[CH];  // f32 skip, or the s16 residual accumulator as a float (exact)
-      if (pre) {
+      // loads were issued during the previous item's last chunk (else here,
+      // before waiting for the MMAs), each later chunk's while the previous
+      // one is finished (HBM latency off the critical path)
+      const bool pre = has_skip && valid;
+      const long long skb = fbase + (long long)(nt * BN) * oplane;
+      // BN = 64 kernels (576 threads at the register cap) keep the plain f32
+      // form: measured faster than the raw-bit / one-item-ahead variant there
+      float sk[CH];
+      if constexpr (BN >= 128) {
+        if (pre && !skr_ready) load_skip(skb, skr);
+        skr_ready = false;
+      } else if (pre) {
         uint32_t off = 0;
-        if (p.skip16) {
 #pragma unroll
-          for (int j = 0; j < CH; ++j, off += ostride) sk[j] = (float)__ldg(skp16 + off);
-        } else {
-#pragma unroll
-          for (int j = 0; j < CH; ++j, off += ostride) sk[j] = __ldg(skp + off);
-        }
+        for (int j = 0; j < CH; ++j, off += ostride) sk[j] = __ldg(p.skip + skb + off);
       }
       if (p.dbg & 1024)
         sm100::mbar_wait(&a_full[acc], (it / kAcc) & 1);
@@ -481,12 +512,14 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
           continue;
         }
         if constexpr (MT >= 2) continue;  // MT > 1 kernels: integer epilogue only (host-checked)
-        if (p.aout) {  // downsample: exact s16 accumulators (|acc| <= 2K < 2^15, host-checked)
-          int16_t* ob = p.aout + fbase + (long long)n0 * oplane;
-          uint32_t off = 0;
+        if constexpr (BN >= 128) {
+          if (p.aout) {  // downsample: exact s16 accumulators (|acc| <= 2K < 2^15, host-checked)
+            int16_t* ob = p.aout + fbase + (long long)n0 * oplane;
+            uint32_t off = 0;
 #pragma unroll
-          for (int j = 0; j < CH; ++j, off += ostride) ob[off] = (int16_t)(int32_t)r[j];
-          continue;
+            for (int j = 0; j < CH; ++j, off += ostride) ob[off] = (int16_t)(int32_t)r[j];
+            continue;
+          }
         }
         const float4* eg = reinterpret_cast<const float4*>(ep + n0);
         const int n4 = p.N / 4;
@@ -510,7 +543,18 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
               v[4 * j + i] = __fmaf_rn(gs[i], __fmul_rn(p.out_scale, (float)(int32_t)r[4 * j + i]), bs[i]);
           }
         }
-        if (pre) {  // NCHW: lanes = consecutive positions -> coalesced per channel
+        if constexpr (BN < 128) {
+          if (pre) {  // NCHW: lanes = consecutive positions -> coalesced per channel
+#pragma unroll
+            for (int j = 0; j < CH; ++j) v[j] += sk[j];
+            if (c0 + CH < BN) {
+              const float* sb = p.skip + skb + (size_t)(c0 + CH) * ostride;
+              uint32_t off = 0;
+#pragma unroll
+              for (int j = 0; j < CH; ++j, off += ostride) sk[j] = __ldg(sb + off);
+            }
+          }
+        } else if (pre) {  // NCHW: lanes = consecutive positions -> coalesced per channel
           if (p.skip16) {
             // the downsample conv's own epilogue, R:linalg.hpp:322-323 (fmul(1, x) == x)
             const float4* sg = reinterpret_cast<const float4*>(ep + 2 * p.N + n0);
@@ -520,22 +564,23 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
               const float gs[4] = {g.x, g.y, g.z, g.w}, bs[4] = {bb.x, bb.y, bb.z, bb.w};
 #pragma unroll
               for (int i = 0; i < 4; ++i)
-                v[4 * j + i] += __fmaf_rn(gs[i], __fmul_rn(p.sk_scale, sk[4 * j + i]), bs[i]);
+                v[4 * j + i] += __fmaf_rn(gs[i], __fmul_rn(p.sk_scale, (float)(int32_t)skr[4 * j + i]), bs[i]);
             }
           } else {
 #pragma unroll
-            for (int j = 0; j < CH; ++j) v[j] += sk[j];
+            for (int j = 0; j < CH; ++j) v[j] += __uint_as_float(skr[j]);
           }
           if (c0 + CH < BN) {
-            uint32_t off = 0;
-            if (p.skip16) {
-              const int16_t* sb = skp16 + (size_t)(c0 + CH) * ostride;
-#pragma unroll
-              for (int j = 0; j < CH; ++j, off += ostride) sk[j] = (float)__ldg(sb + off);
-            } else {
-              const float* sb = skp + (size_t)(c0 + CH) * ostride;
-#pragma unroll
-              for (int j = 0; j < CH; ++j, off += ostride) sk[j] = __ldg(sb + off);
+            load_skip(skb + (long long)(c0 + CH) * ostride, skr);
+          } else {
+            // last chunk: this group's next item's first chunk, one item ahead
+            const int nxt = item + (G / MT) * (int)gridDim.x;
+            if (nxt < n_items) {
+              const long long nb = skip_at(nxt);
+              if (nb >= 0) {
+                load_skip(nb, skr);
+                skr_ready = true;
+              }
             }
           }
         }
@@ -1286,12 +1331,17 @@ int setup_fused(tk_net* net) {
       k.skip16 = nullptr;
       k.sk_gain = k.sk_bias = nullptr;
       k.sk_scale = 1.0f;
-      if (!f32_residual_forced() && cv.is_down && s16_ok(cv)) {  // (its f32 tensor holds the s16 values)
+      // (the s16 residual path is compiled into the BN >= 128 kernels only)
+      auto s16_pair = [&](const Conv& dv) {
+        return !f32_residual_forced() && s16_ok(dv) && dv.d.out_c >= 128 && cvs.back().d.out_c >= 128 &&
+               !getenv("TK_CONV_BNMAX");
+      };
+      if (cv.is_down && s16_pair(cv)) {  // (its f32 tensor holds the s16 values)
         k.aout = reinterpret_cast<int16_t*>(k.fout);
         k.fout = nullptr;
-      } else if (!f32_residual_forced() && cv.skip_f >= 0) {
+      } else if (cv.skip_f >= 0) {
         for (auto& dv : cvs)
-          if (dv.is_down && dv.out_f == cv.skip_f && s16_ok(dv)) {
+          if (dv.is_down && dv.out_f == cv.skip_f && s16_pair(dv)) {
             k.skip16 = reinterpret_cast<const int16_t*>(k.skip);
             k.skip = nullptr;
             k.sk_gain = dv.d_gain;
