@@ -710,6 +710,61 @@ __global__ void k_pack_input(const PackIn p) {
   }
 }
 
+// Same result, one thread per (image, position) walking all C channels:
+// 32-bit index math (N*H*W < 2^31, host-checked), every 16-channel group's
+// loads in flight together, and each variant's R-byte position row written
+// whole by one thread (full 32-byte sectors instead of 16-byte pieces from
+// four different warps).
+__global__ void __launch_bounds__(256) k_pack_input_rows(const PackIn p) {
+  const int HW = p.H * p.W;
+  const int total = p.N * HW;
+  const int groups = p.C / 16;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int n = i / HW, pix = i - n * HW;
+    const int y = pix / p.W, xx = pix - y * p.W;
+    const int py = y + 1, px = xx + 1;
+    const long long P1 = ((long long)n * p.Hp + py) * p.Wp + px;
+    const long long P4 = ((long long)n * p.PH + (py >> 1)) * p.PW + (px >> 1);
+    const int ph4 = (py & 1) * 2 + (px & 1);
+#pragma unroll 4
+    for (int g = 0; g < groups; ++g) {
+      const float* src = p.x + ((long long)n * p.C + g * 16) * HW + pix;
+      float v[16];
+      bool bad = false;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        v[j] = __ldg(src + (long long)j * HW);
+        bad |= !(v[j] >= 0.0f && v[j] <= 3.402823466e38f);
+      }
+      if (bad) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int e = tk_error_code(v[j], 1);
+          if (e != TK_OK) tk_raise(p.err, (unsigned long long)(((long long)n * p.C + g * 16 + j) * HW + pix), e);
+        }
+      }
+      for (int o = 0; o < p.n_q; ++o) {
+        uint32_t w[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          uint32_t b = 0;
+#pragma unroll
+          for (int i2 = 0; i2 < 4; ++i2) {
+            const float xv = v[4 * j + i2];
+            b |= ((uint32_t)(xv > p.t0[o]) + (uint32_t)(xv > p.t1[o])) << (8 * i2);
+          }
+          w[j] = b;
+        }
+        const int Rq = p.q_R[o];
+        const int c0 = g * 16, chq = c0 / Rq, cq = c0 - chq * Rq;
+        const long long off = p.q_phases[o] == 4 ? ((long long)(chq * 4 + ph4) * p.q_pos[o] + P4) * Rq + cq
+                                                 : ((long long)chq * p.q_pos[o] + P1) * Rq + cq;
+        *reinterpret_cast<uint4*>(p.q[o] + off) = make_uint4(w[0], w[1], w[2], w[3]);
+      }
+    }
+  }
+}
+
 // generic path helpers (NCHW)
 __global__ void k_residual_relu(float* __restrict__ z, const float* __restrict__ sc, long long n, int relu_only) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
@@ -1710,8 +1765,14 @@ int tk_net_forward(tk_context* ctx, tk_net* net, const float* x, float* out, flo
   if (net->fused) {
     PackIn pk = net->pack;
     pk.x = x;
-    const long long total = (long long)pk.N * (pk.C / 16) * pk.H * pk.W;
-    k_pack_input<<<(unsigned)std::min<long long>((total + 255) / 256, 148 * 64), 256, 0, s>>>(pk);
+    const long long rows = (long long)pk.N * pk.H * pk.W;
+    static const bool old_pack = getenv("TK_PACK_INPUT_OLD") != nullptr;  // A/B
+    if (rows < (1ll << 31) && !old_pack) {
+      k_pack_input_rows<<<(unsigned)std::min<long long>((rows + 255) / 256, 148 * 16), 256, 0, s>>>(pk);
+    } else {
+      const long long total = rows * (pk.C / 16);
+      k_pack_input<<<(unsigned)std::min<long long>((total + 255) / 256, 148 * 64), 256, 0, s>>>(pk);
+    }
     if (cudaGetLastError() != cudaSuccess) return TK_ERR_CUDA;
     int ci = 0;
     for (const auto& cvs : net->convs)
