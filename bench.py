@@ -722,6 +722,10 @@ def run_reference(args) -> None:
     else:
         from paper_2008_05101_b200.resnet import reference_cpu_run
         line = reference_cpu_run(args, METRIC, threads)
+    # the run this line stands beside: the same --gpus N launch; the reference
+    # itself computes on rank 0's host cores
+    line["n_gpus"] = args.gpus
+    line["device"] = f"host CPU, {threads} threads (rank 0 only)"
     print(json.dumps(line), flush=True)
 
 
