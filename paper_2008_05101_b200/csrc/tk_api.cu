@@ -83,17 +83,6 @@ void* tk_workspace(tk_context* ctx, size_t bytes) {
   return ctx->ws;
 }
 
-void* tk_red_workspace(tk_context* ctx, size_t bytes) {
-  if (bytes <= ctx->red_bytes) return ctx->red_ws;
-  cudaDeviceSynchronize();
-  if (ctx->red_ws) cudaFree(ctx->red_ws);
-  ctx->red_ws = nullptr;
-  ctx->red_bytes = 0;
-  if (cudaMalloc(&ctx->red_ws, bytes) != cudaSuccess) return nullptr;
-  ctx->red_bytes = bytes;
-  return ctx->red_ws;
-}
-
 extern "C" {
 
 int tk_version(void) { return 100; }
@@ -158,7 +147,6 @@ int tk_context_destroy(tk_context* ctx) {
   if (!ctx) return TK_OK;
   cudaDeviceSynchronize();
   if (ctx->ws) cudaFree(ctx->ws);
-  if (ctx->red_ws) cudaFree(ctx->red_ws);
   if (ctx->d_err) cudaFree(ctx->d_err);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   delete ctx;

@@ -21,8 +21,6 @@ struct tk_context {
   void* ws = nullptr;                   // scratch, grown on demand
   size_t ws_bytes = 0;
   void* pinned = nullptr;               // 8-byte host slot for the error word
-  void* red_ws = nullptr;               // split-K partial slices of the TC GEMM
-  size_t red_bytes = 0;
 };
 
 struct tk_layer {
@@ -81,7 +79,6 @@ __device__ __forceinline__ int tk_error_code(float p, int nonneg) {
 // host helpers implemented in tk_api.cu
 int tk_make_qparams(float a1, float a2, int mode, tk_qparams* q);
 void* tk_workspace(tk_context* ctx, size_t bytes);
-void* tk_red_workspace(tk_context* ctx, size_t bytes);
 
 // launchers (tk_codec.cu)
 cudaError_t tk_launch_quantize_pack(const float* x, size_t rows, size_t n,

@@ -77,7 +77,7 @@ template <int BN, bool F4>
 __global__ void __launch_bounds__(kThreads, 1)
 k_gemm_tc_i8(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
              const __grid_constant__ CUtensorMap tmO, int direct, int mcx,
-             int M, int N, int num_kb, int m_pad, int n_pad, int S, int16_t* __restrict__ red, tk_epilogue e,
+             int M, int N, int num_kb, int m_pad, int n_pad, int S, tk_epilogue e,
              int dbg) {
   constexpr int kStages = TcSmem<BN>::kStages;
   extern __shared__ uint8_t smem_raw[];
@@ -456,10 +456,6 @@ k_gemm_tc_i8(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
         }
       }
       const int nv = N - n < 8 ? N - n : 8;
-      if (dbg & 64) {  // profiling: reduction without the output stores
-        if ((acc[0] ^ acc[7]) == 0x7fffffff) red[0] = 1;
-        continue;
-      }
       if (e.mode == TK_EPI_I32) {
         int32_t* o = static_cast<int32_t*>(e.out) + (size_t)m * N + n;
         if (vec_ok) {
@@ -549,7 +545,7 @@ bool make_out_map(CUtensorMap* m, void* base, uint64_t rows, uint64_t cols, bool
 
 template <int BN, bool F4>
 cudaError_t launch(const int8_t* a, int M, int num_kb, const tk_layer* L, tk_epilogue e, int S,
-                   bool row_major, int16_t* red, cudaStream_t s) {
+                   bool row_major, cudaStream_t s) {
   CUtensorMap ta, tb, to;
   // Row-major, 16-byte aligned outputs go out through TMA tensor stores:
   // directly from TMEM when S == 1, after the cluster reduction when S = 2, 4.
@@ -593,7 +589,7 @@ cudaError_t launch(const int8_t* a, int M, int num_kb, const tk_layer* L, tk_epi
   static const int dbg0 = getenv("TK_GEMM_DBG") ? atoi(getenv("TK_GEMM_DBG")) : 0;  // profiling knob
   static int launches = 0;
   const int dbg = (dbg0 & 16) ? (dbg0 | ((launches++ & 1) << 8)) : dbg0;  // stamp buffer parity
-  return cudaLaunchKernelEx(&cfg, k_gemm_tc_i8<BN, F4>, ta, tb, to, direct, mcx, M, L->out_c, num_kb, m_pad, L->n_pad, S, red, e,
+  return cudaLaunchKernelEx(&cfg, k_gemm_tc_i8<BN, F4>, ta, tb, to, direct, mcx, M, L->out_c, num_kb, m_pad, L->n_pad, S, e,
                             dbg);
 }
 
@@ -645,15 +641,14 @@ cudaError_t tk_launch_gemm_tc_fmt(const int8_t* a_s8, int M, int k_pad, const tk
   if (!(row_major && S == 1))
     while ((num_kb + S - 1) / S > max_kb && S < 8) S *= 2;
   if (!(row_major && S == 1) && (num_kb + S - 1) / S > max_kb) return cudaErrorNotSupported;
-  int16_t* red = nullptr;  // (split-K exchange runs through distributed shared memory)
   if (fp4) {
-    if (BN == 256) return launch<256, true>(a_s8, M, num_kb, L, e, S, row_major, red, s);
-    if (BN == 128) return launch<128, true>(a_s8, M, num_kb, L, e, S, row_major, red, s);
-    return launch<64, true>(a_s8, M, num_kb, L, e, S, row_major, red, s);
+    if (BN == 256) return launch<256, true>(a_s8, M, num_kb, L, e, S, row_major, s);
+    if (BN == 128) return launch<128, true>(a_s8, M, num_kb, L, e, S, row_major, s);
+    return launch<64, true>(a_s8, M, num_kb, L, e, S, row_major, s);
   }
-  if (BN == 256) return launch<256, false>(a_s8, M, num_kb, L, e, S, row_major, red, s);
-  if (BN == 128) return launch<128, false>(a_s8, M, num_kb, L, e, S, row_major, red, s);
-  return launch<64, false>(a_s8, M, num_kb, L, e, S, row_major, red, s);
+  if (BN == 256) return launch<256, false>(a_s8, M, num_kb, L, e, S, row_major, s);
+  if (BN == 128) return launch<128, false>(a_s8, M, num_kb, L, e, S, row_major, s);
+  return launch<64, false>(a_s8, M, num_kb, L, e, S, row_major, s);
 }
 
 int tk_debug_gemm_stamps(unsigned long long* host_out) {
