@@ -239,3 +239,29 @@ def test_fp4_symmetric_levels(tk):
     want = lv.astype(np.int64) @ wq.T.astype(np.int64)
     assert np.array_equal(tk.gemm_levels(a4, layer).cpu().numpy(), want)
     assert np.array_equal(tk.gemm_levels(a8, layer).cpu().numpy(), want)
+
+
+def test_fp4_operand_errors_and_stream_order(tk):
+    """FP4 entry points: K padding must be a multiple of 256 (the FP4 K block);
+    GEMMs launched as programmatic dependents stay ordered behind the kernels
+    that produce their operands and read their outputs (repeated FC calls on
+    one stream, each consuming the previous output)."""
+    rng = np.random.default_rng(81)
+    k, n = 512, 512
+    wq = rng.integers(-1, 2, (n, k)).astype(np.int8)
+    layer = _layer(tk, wq, k, n, 1, 1, 0, ta=(0.5, 0.9), gain=(rng.uniform(0.5, 1.5, n) / 32).astype(np.float32),
+                   bias=np.zeros(n, np.float32))
+    x = torch.from_numpy(np.abs(rng.standard_normal((256, k))).astype(np.float32)).cuda()
+    with pytest.raises(tk.InvalidArgument):
+        tk.quantize_levels(x, tk.QuantThresholds(0.5, 0.9), tk.QuantMode.kActivationNonneg, 384, "fp4")
+    assert tk.layer_k_pad(layer, "fp4") % 256 == 0
+    # chain: y_{i+1} = FC(relu(y_i)) on the FP4 pipe vs the POPC pipe, no host syncs in between
+    outs = {}
+    for be in (tk.Backend.TC_F4, tk.Backend.POPC):
+        layer.set_backend(be)
+        y = x
+        for _ in range(4):
+            y = torch.relu(tk.fully_connected_ternary(y, 256, layer, check_errors=False))
+        torch.cuda.synchronize()
+        outs[be.name] = y.cpu().numpy()
+    assert np.array_equal(outs["TC_F4"].view(np.int32), outs["POPC"].view(np.int32))

@@ -1,0 +1,57 @@
+"""Event timeline of one pipelined ResNet e2e step (copy stream vs compute
+stream), relative to the step start (ms)."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+from paper_2008_05101_b200.resnet import ResNetWorkload  # noqa: E402
+
+
+def main():
+    w = ResNetWorkload(os.environ.get("W", "resnet18"))
+    pipe = w.pipe
+    for _ in range(3):
+        w.step_e2e()
+    torch.cuda.synchronize()
+    cs = torch.cuda.current_stream()
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    t0 = ev()
+    t0.record(cs)
+    marks = []
+    pipe.copy_stream.wait_stream(cs)
+    with torch.cuda.stream(pipe.copy_stream):
+        for i in range(pipe.chunks):
+            pipe.copy_stream.wait_event(pipe.ev_consumed[i])
+            pipe.img[i].copy_(w.images_host[i * pipe.cb:(i + 1) * pipe.cb], non_blocking=True)
+            pipe.ev_copied[i].record(pipe.copy_stream)
+            e = ev()
+            e.record(pipe.copy_stream)
+            marks.append((f"h2d {i} done", e))
+    i = 0
+    for gi, g in enumerate(pipe.groups):
+        for k in range(g):
+            cs.wait_event(pipe.ev_copied[i])
+            pipe.net.stem(pipe.img[i], out=pipe.xg[gi][k * pipe.cb:(k + 1) * pipe.cb])
+            pipe.ev_consumed[i].record(cs)
+            e = ev()
+            e.record(cs)
+            marks.append((f"stem {i} done", e))
+            i += 1
+        lo = (i - g) * pipe.cb
+        pipe.bodies[g].forward(pipe.xg[gi], pooled=pipe.pooled[lo:lo + g * pipe.cb], check_errors=False)
+        e = ev()
+        e.record(cs)
+        marks.append((f"body group {gi} ({g} slices) done", e))
+    pipe.net.head(pipe.pooled, out=pipe.logits)
+    e = ev()
+    e.record(cs)
+    marks.append(("head done", e))
+    torch.cuda.synchronize()
+    for name, e in sorted(marks, key=lambda m: t0.elapsed_time(m[1])):
+        print(f"{t0.elapsed_time(e):7.3f} ms  {name}")
+
+
+if __name__ == "__main__":
+    main()
