@@ -34,6 +34,8 @@
 #include <mutex>
 #include <vector>
 
+#include <cstdio>
+
 #include "tk_internal.cuh"
 #include "tk_sm100.cuh"
 
@@ -1789,7 +1791,10 @@ int tk_net_forward(tk_context* ctx, tk_net* net, const float* x, float* out, flo
     for (const auto& cvs : net->convs)
       for (const auto& cv : cvs) {
         if (net->timing) cudaEventRecord(net->ev[2 * ci], s);
-        if (run_conv(cv, x, s) != cudaSuccess) return TK_ERR_CUDA;
+        if (const cudaError_t ce = run_conv(cv, x, s); ce != cudaSuccess) {
+          if (getenv("TK_NET_DEBUG")) fprintf(stderr, "tk_net_forward: conv %d: %s\n", ci, cudaGetErrorString(ce));
+          return TK_ERR_CUDA;
+        }
         if (net->timing) cudaEventRecord(net->ev[2 * ci + 1], s);
         ++ci;
       }
