@@ -41,8 +41,11 @@ constexpr int kThreads = 320;
 
 template <int BN>
 struct TcSmem {
-  static constexpr int kA = BM * BK;  // bytes per stage
-  static constexpr int kB = BN * BK;
+  // K blocks per stage: BN = 64 tiles take two per TMA box (3-D box over the
+  // K-block-major planes): fewer, larger requests move more bytes per SM
+  static constexpr int kKD = BN <= 128 ? 2 : 1;
+  static constexpr int kA = kKD * BM * BK;  // bytes per stage
+  static constexpr int kB = kKD * BN * BK;
   static constexpr int kStage = kA + kB;
   // as many stages as ~200 KB of shared memory holds (latency hiding)
   static constexpr int kStages = (200 * 1024 / kStage) > 8 ? 8 : (200 * 1024 / kStage);
@@ -155,26 +158,39 @@ k_gemm_tc_i8(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
     // ---- TMA producer (whole warp waits, lane 0 issues) ----
     // weights do not depend on the previous kernel: the first stages' B
     // boxes go out before griddepcontrol.wait, the A boxes after it
-    const int npre = (dbg & 8) ? 0 : min(kStages, kb1 - kb0);
+    constexpr int KD = TcSmem<BN>::kKD;
+    const int nst = (kb1 - kb0 + KD - 1) / KD;  // stages of this CTA's K range
+    // (a box may reach one K block past kb1: zero fill past num_kb; inside
+    // another split's range the MMA loop skips that block)
+    auto load_b = [&](int s2, int kb) {
+      if constexpr (KD == 1)
+        sm100::tma_load_2d(sB + s2 * TcSmem<BN>::kB, &tmB, &full[s2], 0, kb * n_pad + n0);
+      else
+        sm100::tma_load_3d(sB + s2 * TcSmem<BN>::kB, &tmB, &full[s2], 0, n0, kb);
+    };
+    const int npre = (dbg & 8) ? 0 : min(kStages, nst);
     if (lane == 0)
       for (int i = 0; i < npre; ++i) {
         sm100::mbar_arrive_expect_tx(&full[i], TcSmem<BN>::kStage);
-        sm100::tma_load_2d(sB + i * TcSmem<BN>::kB, &tmB, &full[i], 0, (kb0 + i) * n_pad + n0);
+        load_b(i, kb0 + i * KD);
       }
     sm100::pdl_wait();
     int s = 0, round = 0;
-    for (int kb = kb0; kb < kb1; ++kb) {
+    for (int si = 0; si < nst; ++si) {
+      const int kb = kb0 + si * KD;
       if (round) sm100::mbar_wait(&empty[s], (round - 1) & 1);
       if (lane == 0) {
         if (dbg & 8) {  // profiling: no operand traffic
           sm100::mbar_arrive(&full[s]);
         } else {
-          if (kb - kb0 >= npre) {
+          if (si >= npre) {
             sm100::mbar_arrive_expect_tx(&full[s], TcSmem<BN>::kStage);
-            sm100::tma_load_2d(sB + s * TcSmem<BN>::kB, &tmB, &full[s], 0, kb * n_pad + n0);
+            load_b(s, kb);
           }
-          // K-block-major operands: each box is one contiguous 16 / BN*128 byte block
-          if (mcx > 1) {
+          // K-block-major operands: each box is KD contiguous 16 KB / BN*128 B blocks
+          if constexpr (KD > 1) {
+            sm100::tma_load_3d(sA + s * TcSmem<BN>::kA, &tmA, &full[s], 0, m0, kb);
+          } else if (mcx > 1) {
             const int part = BM / mcx;
             sm100::tma_load_2d_mc(sA + s * TcSmem<BN>::kA + mc_rank * part * 128, &tmA, &full[s], 0,
                                   kb * m_pad + m0 + (int)mc_rank * part, mc_mask);
@@ -187,23 +203,31 @@ k_gemm_tc_i8(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
       if (++s == kStages) { s = 0; ++round; }
     }
   } else if (warp == 1) {
-    // ---- MMA issuer: 4 x (128 x BN x 32) per stage ----
+    // ---- MMA issuer: KD x 4 x (128 x BN x 32 bytes of K) per stage ----
+    constexpr int KD = TcSmem<BN>::kKD;
     constexpr uint32_t idesc = F4 ? sm100::idesc_f4(BM, BN) : sm100::idesc_i8(BM, BN);
+    const int nst = (kb1 - kb0 + KD - 1) / KD;
     int s = 0, round = 0;
-    for (int kb = kb0; kb < kb1; ++kb) {
+    for (int si = 0; si < nst; ++si) {
+      const int kbs = kb0 + si * KD;
       sm100::mbar_wait(&full[s], round & 1);
       sm100::tc_fence_after();
-      const uint32_t a0 = sm100::smem_u32(sA + s * TcSmem<BN>::kA);
-      const uint32_t b0 = sm100::smem_u32(sB + s * TcSmem<BN>::kB);
       if (!(dbg & 4)) {  // dbg & 4: profiling, no MMAs
 #pragma unroll
-        for (int k = 0; k < BK / 32; ++k) {  // 32 bytes per MMA: K = 32 (s8) or 64 (fp4)
-          if constexpr (F4)
-            sm100::mma_f4_elect(tmem, sm100::desc_k_sw128(a0 + k * 32), sm100::desc_k_sw128(b0 + k * 32), idesc,
-                                (kb > kb0 || k > 0) ? 1u : 0u, tmem + BN, tmem + BN + 64);
-          else
-            sm100::mma_i8_elect(tmem, sm100::desc_k_sw128(a0 + k * 32), sm100::desc_k_sw128(b0 + k * 32), idesc,
-                                (kb > kb0 || k > 0) ? 1u : 0u);
+        for (int j = 0; j < KD; ++j) {
+          const int kb = kbs + j;
+          if (kb >= kb1) break;
+          const uint32_t a0 = sm100::smem_u32(sA + s * TcSmem<BN>::kA + j * BM * BK);
+          const uint32_t b0 = sm100::smem_u32(sB + s * TcSmem<BN>::kB + j * BN * BK);
+#pragma unroll
+          for (int k = 0; k < BK / 32; ++k) {  // 32 bytes per MMA: K = 32 (s8) or 64 (fp4)
+            if constexpr (F4)
+              sm100::mma_f4_elect(tmem, sm100::desc_k_sw128(a0 + k * 32), sm100::desc_k_sw128(b0 + k * 32),
+                                  idesc, (kb > kb0 || k > 0) ? 1u : 0u, tmem + BN, tmem + BN + 64);
+            else
+              sm100::mma_i8_elect(tmem, sm100::desc_k_sw128(a0 + k * 32), sm100::desc_k_sw128(b0 + k * 32),
+                                  idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+          }
         }
       }
       if (mcx > 1)
@@ -530,6 +554,19 @@ bool make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, ui
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// 3-D u8 tensor [planes][rows][128 bytes] (K-block-major), box [depth][box_rows][128 bytes]
+bool make_map3(CUtensorMap* m, const void* base, uint64_t rows, uint64_t planes, uint32_t box_rows, uint32_t depth) {
+  EncodeFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[3] = {128, rows, planes};
+  cuuint64_t strides[2] = {128, rows * 128};
+  cuuint32_t box[3] = {128, box_rows, depth};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(base), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // 2-D 4-byte tensor [rows][cols] (row-major output), 32 x 32 boxes, 128B swizzle
 bool make_out_map(CUtensorMap* m, void* base, uint64_t rows, uint64_t cols, bool f32) {
   EncodeFn fn = encode_fn();
@@ -563,8 +600,15 @@ cudaError_t launch(const int8_t* a, int M, int num_kb, const tk_layer* L, tk_epi
     for (int c = 4; c >= 2; c /= 2)
       if (c <= want && n_tiles % c == 0) { mcx = c; break; }
   }
-  if (!make_map(&ta, a, (uint64_t)num_kb * m_pad, 128, BM / mcx)) return cudaErrorInvalidValue;
-  if (!make_map(&tb, F4 ? L->d_w4 : L->d_w8, (uint64_t)num_kb * L->n_pad, 128, BN)) return cudaErrorInvalidValue;
+  if constexpr (TcSmem<BN>::kKD > 1) {  // 3-D view [kb][rows][128 B], boxes of kKD K blocks
+    mcx = 1;
+    if (!make_map3(&ta, a, (uint64_t)m_pad, (uint64_t)num_kb, BM, TcSmem<BN>::kKD)) return cudaErrorInvalidValue;
+    if (!make_map3(&tb, F4 ? L->d_w4 : L->d_w8, (uint64_t)L->n_pad, (uint64_t)num_kb, BN, TcSmem<BN>::kKD))
+      return cudaErrorInvalidValue;
+  } else {
+    if (!make_map(&ta, a, (uint64_t)num_kb * m_pad, 128, BM / mcx)) return cudaErrorInvalidValue;
+    if (!make_map(&tb, F4 ? L->d_w4 : L->d_w8, (uint64_t)num_kb * L->n_pad, 128, BN)) return cudaErrorInvalidValue;
+  }
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(k_gemm_tc_i8<BN, F4>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcSmem<BN>::kBytes);
