@@ -967,23 +967,35 @@ __global__ void k_affine_relu_maxpool4(const float* __restrict__ x, int C, int H
   }
 }
 
-__global__ void k_pool_nchw(const float* __restrict__ x, int NC, int HW, float* __restrict__ out) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= NC) return;
-  const float* src = x + (long long)i * HW;
+// spatial mean -> [NC] (the head input), each plane summed left to right
+// (the reference's order).  A block's planes (one per thread) are one
+// contiguous range: staged through shared memory with coalesced loads, then
+// each thread walks its own plane.
+__global__ void __launch_bounds__(64) k_pool_nchw(const float* __restrict__ x, int NC, int HW,
+                                                  float* __restrict__ out) {
+  extern __shared__ float s_pool[];  // [blockDim.x][HW]
+  const int p0 = blockIdx.x * blockDim.x;
+  const int np = min((int)blockDim.x, NC - p0);
+  const float* src = x + (long long)p0 * HW;
+  for (int i = threadIdx.x; i < np * HW; i += blockDim.x) s_pool[i] = __ldg(src + i);
+  __syncthreads();
+  if ((int)threadIdx.x >= np) return;
+  const float* row = s_pool + threadIdx.x * HW;
   float s = 0.0f;
-  int j = 0;
-  // left-to-right sum (the reference's order); the loads of 8 terms are
-  // issued together so the chain waits on one memory latency per 8 adds
-  for (; j + 8 <= HW; j += 8) {
-    float t[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) t[u] = __ldg(src + j + u);
-#pragma unroll
-    for (int u = 0; u < 8; ++u) s += t[u];
+  for (int j = 0; j < HW; ++j) s += row[j];
+  out[p0 + threadIdx.x] = s / (float)HW;
+}
+
+void pool_nchw(const float* x, int NC, int HW, float* out, cudaStream_t s) {
+  // planes per block: up to 64, within 96 KB of staged floats
+  const int planes = std::max(1, std::min(64, (96 * 1024) / (HW * 4)));
+  const size_t smem = (size_t)planes * HW * 4;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_pool_nchw, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024 + 4096);
+    attr = true;
   }
-  for (; j < HW; ++j) s += __ldg(src + j);
-  out[i] = s / (float)HW;
+  k_pool_nchw<<<(NC + planes - 1) / planes, planes, smem, s>>>(x, NC, HW, out);
 }
 
 // ---------------------------------------------------------------------------
@@ -1801,7 +1813,7 @@ int tk_net_forward(tk_context* ctx, tk_net* net, const float* x, float* out, flo
     const F32T& f = net->f32[net->final_f];
     if (out) cudaMemcpyAsync(out, f.p, (size_t)f.elems * 4, cudaMemcpyDeviceToDevice, s);
     if (pooled)
-      k_pool_nchw<<<(net->batch * f.C + 255) / 256, 256, 0, s>>>(f.p, net->batch * f.C, f.H * f.W, pooled);
+      pool_nchw(f.p, net->batch * f.C, f.H * f.W, pooled, s);
     return cudaGetLastError() == cudaSuccess ? TK_OK : TK_ERR_CUDA;
   }
   // generic: NCHW floats through conv2d_ternary (R:linalg.hpp:301-328)
@@ -1845,7 +1857,7 @@ int tk_net_forward(tk_context* ctx, tk_net* net, const float* x, float* out, flo
   const long long total = (long long)net->batch * net->out_c * H * W;
   if (out) cudaMemcpyAsync(out, cur, total * 4, cudaMemcpyDeviceToDevice, s);
   if (pooled)
-    k_pool_nchw<<<(net->batch * net->out_c + 255) / 256, 256, 0, s>>>(cur, net->batch * net->out_c, H * W, pooled);
+    pool_nchw(cur, net->batch * net->out_c, H * W, pooled, s);
   return cudaGetLastError() == cudaSuccess ? TK_OK : TK_ERR_CUDA;
 }
 
