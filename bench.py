@@ -497,7 +497,7 @@ class ConvWorkload:
         best = min(self.pipe_ms, key=self.pipe_ms.get)
         self.backend = tk.Backend[best]
         self.layer.set_backend(self.backend)
-        self.launches_per_step = 2 if self.backend == tk.Backend.POPC else 3
+        self.launches_per_step = 2  # im2col (fused with the level expansion on the TC pipes) + GEMM
         self.config = {"workload": "cfg2 ternary 3x3 conv 64->64, 56x56, batch 1 (conv2d_ternary: "
                                    "pack-fused im2col -> ternary GEMM -> folded BN)",
                        "batch": batch, "in_c": c, "out_c": c, "hw": hw, "gemm_m_n_k": [M, c, 9 * c],

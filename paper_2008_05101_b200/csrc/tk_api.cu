@@ -417,15 +417,13 @@ int tk_conv2d_ternary(tk_context* ctx, const tk_layer* L, const float* x,
   const int be = tk_layer_get_backend(L, (int)M);
   const size_t rows_bytes = M * L->wpr64 * 8;
   if (tc_backend(be) && tk_tc_supported((int)M, L->out_c, L->k_pad)) {
+    // im2col + quantize + level expansion in one kernel, then the GEMM
     const bool f4 = be == TK_BACKEND_TC_F4;
     const size_t m_pad = (M + 127) / 128 * 128;
-    char* ws = (char*)tk_workspace(ctx, rows_bytes + tc_operand_bytes(L, m_pad, f4) + 256);
-    if (!ws) return TK_ERR_CUDA;
-    uint64_t* rows = (uint64_t*)ws;
-    int8_t* a8 = (int8_t*)(ws + ((rows_bytes + 255) / 256) * 256);
-    TK_CUDA(tk_launch_im2col(x, n, L->in_c, h, w, L->kh, L->kw, L->stride, L->pad,
-                             q, rows, ctx->d_err, s));
-    TK_CUDA(tk_launch_expand_rows(rows, M, L->wpr64, L->nonneg, tc_k_pad(L, f4), f4, a8, s));
+    int8_t* a8 = (int8_t*)tk_workspace(ctx, tc_operand_bytes(L, m_pad, f4));
+    if (!a8) return TK_ERR_CUDA;
+    TK_CUDA(tk_launch_im2col_levels(x, n, L->in_c, h, w, L->kh, L->kw, L->stride, L->pad, q, L->nonneg,
+                                    tc_k_pad(L, f4), f4, a8, ctx->d_err, s));
     TK_CUDA(tk_launch_gemm_tc_fmt(a8, (int)M, tc_k_pad(L, f4), L, e, f4, s));
     return TK_OK;
   }

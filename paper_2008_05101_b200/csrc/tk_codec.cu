@@ -200,6 +200,74 @@ __global__ void k_expand_rows_s8(const uint32_t* __restrict__ rows,
   }
 }
 
+// im2col_quantize_pack fused with the level expansion: f32 NCHW input ->
+// the tensor-core level operand in one pass (the packed 2-bit rows of
+// k_im2col are formed in registers with the same quantizer and error
+// checks, then expanded like k_expand_rows_s8).  Chunks past the packed
+// row (up to k_pad) are written as zero levels.
+template <bool F4>
+__global__ void k_im2col_levels(const float* __restrict__ x, int n, int c, int h, int w, int kh, int kw, int stride,
+                                int pad, int oh, int ow, int K, int w32pr, tk_qparams q, int offset, int k_pad,
+                                size_t m_pad, int8_t* __restrict__ out, unsigned long long* err) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // (the GEMM waits for this grid)
+  const size_t rows = (size_t)n * oh * ow;
+  const int chunks = k_pad / 16;
+  const size_t total = rows * (size_t)chunks;
+  const uint32_t tbl = offset ? 0x02010100u : 0x010000FFu;
+  const uint32_t ntbl = offset ? 0x4220u : 0x200Au;
+  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total; t += (size_t)gridDim.x * blockDim.x) {
+    const size_t r = t / chunks;
+    const int j = (int)(t - r * chunks);
+    uint32_t wd = 0;
+    const bool have = j < w32pr;
+    if (have) {
+      const int b = (int)(r / ((size_t)oh * ow));
+      const int p = (int)(r - (size_t)b * oh * ow);
+      const int oy = p / ow, ox = p - (p / ow) * ow;
+      const int l0 = j * 16;
+      const int valid = l0 >= K ? 0 : min(16, K - l0);
+      int kpos = l0 / c, ci = l0 - kpos * c;
+      int ky = kpos / kw, kx = kpos - ky * kw;
+      const float* img = x + (size_t)b * c * h * w;
+      float v[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        float val = 0.0f;
+        if (i < valid) {
+          const int iy = oy * stride - pad + ky, ix = ox * stride - pad + kx;
+          if (iy >= 0 && iy < h && ix >= 0 && ix < w) val = __ldg(img + ((size_t)ci * h + iy) * w + ix);
+          if (++ci == c) {
+            ci = 0;
+            if (++kx == kw) { kx = 0; ++ky; }
+          }
+        }
+        v[i] = val;
+      }
+      wd = lane_word16(v, valid, q, err, r * (size_t)K + l0);
+    }
+    if constexpr (F4) {
+      uint2 o = make_uint2(0, 0);
+      if (have) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const uint32_t nib = (ntbl >> (4 * ((wd >> (2 * i)) & 3u))) & 0xFu;
+          if (i < 8) o.x |= nib << (4 * i); else o.y |= nib << (4 * (i - 8));
+        }
+      }
+      store_chunk_f4(out, m_pad, r, j, o);
+    } else {
+      uint4 o = make_uint4(0, 0, 0, 0);
+      if (have) {
+        o.x = expand4(wd & 0xFF, tbl);
+        o.y = expand4((wd >> 8) & 0xFF, tbl);
+        o.z = expand4((wd >> 16) & 0xFF, tbl);
+        o.w = expand4(wd >> 24, tbl);
+      }
+      reinterpret_cast<uint4*>(out + ((size_t)(j >> 3) * m_pad + r) * 128)[j & 7] = o;
+    }
+  }
+}
+
 // Floats -> s8 quantization levels ({0,1,2} activation, {-1,0,1} weight
 // mode) for the tensor-core FC path; columns >= n are zero.
 template <bool F4>
@@ -280,6 +348,22 @@ cudaError_t tk_launch_quantize_pack(const float* x, size_t rows, size_t n,
   const bool vec4 = (n % 4 == 0) && ((uintptr_t)x % 16 == 0);
   k_quantize_pack<<<grid_for(total), kThreads, 0, s>>>(
       x, rows, n, w32pr, q, reinterpret_cast<uint32_t*>(words), err, vec4);
+  return cudaGetLastError();
+}
+
+cudaError_t tk_launch_im2col_levels(const float* x, int n, int c, int h, int w, int kh, int kw, int stride, int pad,
+                                    tk_qparams q, int offset, int k_pad, bool fp4, int8_t* out,
+                                    unsigned long long* err, cudaStream_t s) {
+  const int oh = (h + 2 * pad - kh) / stride + 1;
+  const int ow = (w + 2 * pad - kw) / stride + 1;
+  const int K = c * kh * kw;
+  const int w32pr = 2 * ((K + 31) / 32);
+  const size_t rows = (size_t)n * oh * ow;
+  const size_t total = rows * (size_t)(k_pad / 16);
+  if (total == 0) return cudaSuccess;
+  const size_t m_pad = (rows + 127) / 128 * 128;
+  (fp4 ? k_im2col_levels<true> : k_im2col_levels<false>)<<<grid_for(total), kThreads, 0, s>>>(
+      x, n, c, h, w, kh, kw, stride, pad, oh, ow, K, w32pr, q, offset, k_pad, m_pad, out, err);
   return cudaGetLastError();
 }
 

@@ -101,6 +101,10 @@ cudaError_t tk_launch_quantize_s8(const float* x, size_t rows, size_t n,
 // fp4: E2M1 nibbles, [k_pad/256][m_pad][128 B] (k_pad a multiple of 256)
 cudaError_t tk_launch_expand_rows(const uint64_t* rows, size_t row_count, int wpr64, int offset, int k_pad,
                                   bool fp4, int8_t* out, cudaStream_t s);
+// im2col_quantize_pack straight into the level operand (s8 or fp4 layout)
+cudaError_t tk_launch_im2col_levels(const float* x, int n, int c, int h, int w, int kh, int kw, int stride, int pad,
+                                    tk_qparams q, int offset, int k_pad, bool fp4, int8_t* out,
+                                    unsigned long long* err, cudaStream_t s);
 cudaError_t tk_launch_quantize_levels(const float* x, size_t rows, size_t n, tk_qparams q, int k_pad, bool fp4,
                                       int8_t* out, unsigned long long* err, cudaStream_t s);
 
