@@ -348,9 +348,13 @@ int tk_layer_set_backend(tk_layer* L, int backend) {
 int tk_layer_get_backend(const tk_layer* L, int m_rows) {
   if (!L) return TK_ERR_INVALID;
   if (L->backend != TK_BACKEND_AUTO) return L->backend;
-  return tk_tc_supported(m_rows, L->out_c, L->k_pad) && m_rows >= 128
-             ? TK_BACKEND_TC_F4
-             : TK_BACKEND_POPC;
+  if (!(tk_tc_supported(m_rows, L->out_c, L->k_pad) && m_rows >= 128)) return TK_BACKEND_POPC;
+  // FP4 unless its coarser K blocks (256 levels) leave too few K blocks to
+  // split across the SMs when the tile grid alone is small (cfg2 at batch 1:
+  // K = 576 -> 3 FP4 blocks vs 5 s8 blocks, 25 tiles; measured i8 18.5 us vs
+  // fp4 20.5 us per step)
+  const long tiles64 = (long)((m_rows + 127) / 128) * ((L->out_c + 63) / 64);
+  return (tiles64 >= 96 || L->k_pad4 / 256 >= 4) ? TK_BACKEND_TC_F4 : TK_BACKEND_TC_I8;
 }
 
 namespace {
