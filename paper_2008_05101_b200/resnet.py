@@ -302,10 +302,10 @@ class ResNetWorkload:
         self.pooled = torch.empty((batch, self.net.body.out_shape[0]), device="cuda")
         self.logits_host = torch.empty((global_batch if rank == 0 else 0, 1000)).pin_memory()
         # e2e: chunked so the image upload overlaps the compute of earlier chunks
-        # (measured, tools/gpu_e2e.sh, R18 b256: 8 slices with the body on two
-        # halves 3.96 ms; 4 slices, body per slice 4.24 ms)
+        # (measured, tools/gpu_e2e.sh, R18 b256: 8 slices, body on 3 + 5
+        # slices 3.87 ms; on 4 + 4 3.98 ms; 4 slices, body per slice 4.24 ms)
         if batch % 8 == 0 and batch >= 128:
-            chunks, groups = 8, [4, 4]
+            chunks, groups = 8, [3, 5]
         elif batch % 4 == 0 and batch >= 64:
             chunks, groups = 4, [2, 2]
         else:
