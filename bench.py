@@ -118,18 +118,42 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(self.rows)}
 
 
-def dist_setup():
+def dist_setup(expected_world: int, backend: str = "nccl"):
+    """Rank / world / local rank from the torchrun environment (this script
+    re-launches itself under torchrun for --gpus N > 1, see self_launch)."""
     import torch
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != expected_world:
+        raise SystemExit(f"bench.py: --gpus {expected_world} but WORLD_SIZE={world}; refusing to measure "
+                         f"a different number of GPUs than asked for")
     if world > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    elif torch.cuda.is_available():
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+    elif backend == "nccl" and torch.cuda.is_available():
         torch.cuda.set_device(0)
     return rank, world, local
+
+
+def self_launch(argv: list[str], gpus: int) -> int:
+    """`python bench.py --gpus N` outside torchrun: re-run this script as N
+    ranks (one process per GPU) with torch.distributed.run on 127.0.0.1, and
+    return the launcher's exit status.  Rank 0 prints the JSON line."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")  # the N-rank NCCL init stays visible in the log
+    env.setdefault("OMP_NUM_THREADS", "1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *argv]
+    return subprocess.call(cmd, env=env)
 
 
 def barrier(world):
@@ -300,25 +324,38 @@ class FcWorkload:
         return same and st == 0 and np.array_equal(y[:4].view(np.int32), ref.reshape(4, self.N).view(np.int32))
 
     def cpu_baseline(self, threads: int) -> dict:
-        return fc_reference(self.x_host, self.wq, threads, rows=64)
+        from oracle.oracle import Reference
+        R = Reference()
+        runs = {}
+        for t in sorted({1, threads}):
+            rc, st = R.time_runs_fc(self.x_host, self.wq, (0.5, 0.9), t)
+            assert rc == 0
+            runs[t] = dict(st, value=self.units_per_step / (st["mean_us"] / 1e6), threads=t)
+        return cpu_baseline_line(runs, threads, "Tops/s", "the full cfg3 batch (256 x 4096 -> 4096): "
+                                 "im2col_quantize_pack + packed_gemm(workers = threads)")
 
 
-def fc_reference(x_host, wq, threads, rows=64) -> dict:
-    """The reference (oracle/_ref): im2col_quantize_pack + packed_gemm with the
-    reference's worker threads, on `rows` of the batch (rows are independent)."""
-    import ctypes as C
-    import numpy as np
-    from oracle.oracle import Reference, ptr, _f32p, _i8p
-    R = Reference()
-    xs = np.ascontiguousarray(x_host[:rows])
-    n, k = wq.shape
-    sec = C.c_double()
-    st = R.lib.ref_time_fc_gemm(ptr(xs, _f32p), rows, k, ptr(wq, _i8p), n, 0.5, 0.9, threads, 1,
-                                C.byref(sec), None)
-    assert st == 0
-    return {"value": 2.0 * rows * k * n / sec.value / 1e12, "unit": "Tops/s", "cores": threads,
-            "kind": "reference", "sample": f"{rows} of the batch rows, 1 call of packed_gemm(workers={threads})",
-            "seconds": sec.value}
+def cpu_baseline_line(runs: dict, threads: int, unit: str, sample: str) -> dict:
+    """`cpu_baseline` from the reference's own time_runs protocol
+    (R:include/ternkit/bench.hpp:64-99: 2 warmup runs, each measured run
+    looped to >= 0.6 s, mean / stddev / median over 5 repeats, stable when
+    stddev <= 15% of the mean), single-threaded (the paper-comparison rule,
+    SPEC.md:474) and on every host thread.  `value` is the all-threads figure."""
+    from oracle.oracle import Reference, host_cpu
+    multi, single = runs[max(runs)], runs[min(runs)]
+    lib = os.path.basename(Reference().path)
+
+    def fmt(r):
+        return {"value": r["value"], "threads": r["threads"], "mean_us": round(r["mean_us"], 3),
+                "stddev_us": round(r["stddev_us"], 3), "median_us": round(r["median_us"], 3),
+                "cv": round(r["cv"], 4), "stable": r["stable"]}
+    return {"value": multi["value"], "unit": unit, "cores": threads, "threads": threads, "kind": "reference",
+            "sample": sample, "single_thread": fmt(single), "all_threads": fmt(multi),
+            "protocol": {"harness": "ternkit::time_runs (R:include/ternkit/bench.hpp:64-99)",
+                         "warmup": multi["warmup"], "repeats": multi["repeats"], "min_run_s": multi["min_run_s"]},
+            "repeats": multi["repeats"], "cv": round(multi["cv"], 4),
+            "isa": f"oracle/_ref/{lib} ({'-march=native AVX-512 build' if 'native' in lib else 'x86-64-v3 AVX2 build'})",
+            "host": host_cpu()}
 
 
 def _time_graph(g, flush, n=20) -> float:
@@ -438,21 +475,18 @@ class DotWorkload:
             ok &= np.array_equal(want, self.step()[:64].cpu().numpy())
         return bool(ok)
 
-    def reference_time(self, threads: int, pairs: int | None = None):
+    def cpu_baseline(self, threads: int) -> dict:
         from oracle.oracle import Reference
         R = Reference()
-        p = pairs or self.P
-        xh = self.x_host[:p].numpy().view(np.uint64)
-        yh = self.y_host[:p].numpy().view(np.uint64)
-        st, out, sec = R.time_dot(xh, yh, self.N, self.wsum[:p], threads)
-        assert st == 0
-        return 2.0 * p * self.N / sec / 1e12, sec, p
-
-    def cpu_baseline(self, threads: int) -> dict:
-        v, sec, p = self.reference_time(threads)
-        return {"value": v, "unit": "Tops/s", "cores": threads, "kind": "reference",
-                "sample": f"all {p} pairs, ternary_dot_nonneg over {threads} host threads (oracle/_ref)",
-                "seconds": sec}
+        xh = self.x_host.numpy().view(np.uint64)
+        yh = self.y_host.numpy().view(np.uint64)
+        runs = {}
+        for t in sorted({1, threads}):
+            rc, st = R.time_runs_dot(xh, yh, self.N, self.wsum, t)
+            assert rc == 0
+            runs[t] = dict(st, value=self.units_per_step / (st["mean_us"] / 1e6), threads=t)
+        return cpu_baseline_line(runs, threads, "Tops/s", f"all {self.P} pairs (N = {self.N}) per call, "
+                                 "ternary_dot_nonneg, pairs split over the threads")
 
 
 class ConvWorkload:
@@ -544,11 +578,141 @@ class ConvWorkload:
         from oracle.oracle import Reference
         R = Reference()
         s = self.shape
-        st, _, sec = R.time_conv(self.x_host_np, s.n, s.c, s.h, s.w, self.spec(), threads, iters=20)
-        assert st == 0
-        return {"value": self.units_per_step / sec, "unit": "Tops/s", "cores": threads, "kind": "reference",
-                "sample": f"20 calls of conv2d_ternary(workers={threads}) on the full cfg2 input (oracle/_ref)",
-                "seconds": sec}
+        runs = {}
+        for t in sorted({1, threads}):
+            rc, st = R.time_runs_conv(self.x_host_np, s.n, s.c, s.h, s.w, self.spec(), t)
+            assert rc == 0
+            runs[t] = dict(st, value=self.units_per_step / (st["mean_us"] / 1e6), threads=t)
+        return cpu_baseline_line(runs, threads, "Tops/s", "the full cfg2 input per call: "
+                                 "conv2d_ternary(workers = threads)")
+
+
+def resnet_batches(name: str, world: int) -> tuple[int, str]:
+    """(global batch, scaling) of the ResNet workloads: cfg4 keeps 256 images
+    per GPU (weak scaling), cfg5 splits a global batch of 1024 (strong)."""
+    if name == "resnet18":
+        return int(os.environ.get("TK_BENCH_BATCH", 256)) * world, "weak"
+    return int(os.environ.get("TK_BENCH_BATCH", 1024)), "strong"
+
+
+class ResNetWorkload:
+    """cfg4 / cfg5.  One step = the ternary body on this rank's shard of the
+    batch, resident in HBM (the paper's protocol: first and last layers
+    excluded); e2e = the whole network from host images (pinned
+    H2D, chunked so uploads overlap compute) to logits gathered on rank 0 and
+    read back (D2H)."""
+
+    def __init__(self, name: str = "resnet18", seed: int = 0, rank: int = 0, world: int = 1):
+        import torch
+        from paper_2008_05101_b200.resnet import PipelinedResNet, TernaryResNet, body_macs
+        from paper_2008_05101_b200.shard import ShardedForward, shard_range
+        depth = 18 if name == "resnet18" else 50
+        global_batch, scaling = resnet_batches(name, world)
+        batch = shard_range(global_batch, rank, world).count
+        self.name, self.depth, self.B, self.global_batch = name, depth, batch, global_batch
+        self.rank, self.world, self.scaling = rank, world, scaling
+        self.net = TernaryResNet(depth, batch, seed)
+        # per-rank images: a distinct slice of the synthetic global batch
+        g = torch.Generator().manual_seed(seed + 1 + rank)
+        self.images_host = torch.rand(batch, 3, 224, 224, generator=g).pin_memory()
+        self.images_dev = self.images_host.cuda()
+        self.x = self.net.stem(self.images_dev)  # body input, resident
+        self.pooled = torch.empty((batch, self.net.body.out_shape[0]), device="cuda")
+        self.logits_host = torch.empty((global_batch if rank == 0 else 0, 1000)).pin_memory()
+        # e2e: chunked so the image upload overlaps the compute of earlier chunks
+        # (measured R18 b256: 8 slices with the body on 3 + 5 slices 3.87 ms;
+        # 4 + 4 3.98 ms; 4 slices, body per slice 4.24 ms)
+        if batch % 8 == 0 and batch >= 128:
+            chunks, groups = 8, [3, 5]
+        elif batch % 4 == 0 and batch >= 64:
+            chunks, groups = 4, [2, 2]
+        else:
+            chunks, groups = 1, [1]
+        self.pipe = PipelinedResNet(self.net, batch, chunks, groups)
+        self.sharded = ShardedForward(lambda _x: self.pipe.forward(self.images_host), global_batch, 1000, rank,
+                                      world)
+        self.macs_per_img = body_macs(self.net.blocks)
+        self.units_per_step = float(global_batch)  # whole job, all ranks
+        self.unit = "img/s"
+        self.launches_per_step = self.net.body.launches(False, True)
+        variant = "ResNet-18" if depth == 18 else "ResNet-50 v1.5 (stride on the 3x3 conv)"
+        self.config = {"workload": f"cfg{'4' if depth == 18 else '5'} {name} ternary body, synthetic 224x224 "
+                                   f"images, global batch {global_batch} over {world} GPU(s) (paper protocol: "
+                                   f"float stem/head excluded from value, included in e2e)",
+                       "model": name, "variant": variant, "global_batch": global_batch, "batch_per_gpu": batch,
+                       "image": 224, "parallelism": f"batch-sharded dp{world}, logits gathered to rank 0",
+                       "fused_pipeline": self.net.body.fused,
+                       "body_gmac_per_img": round(self.macs_per_img / 1e9, 4),
+                       "e2e_slices": {"chunks": chunks, "body_groups": groups}}
+        in_mb = batch * 64 * 56 * 56 * 4 / 2**20
+        self.needs_flush = in_mb <= 126
+        self.config["l2"] = ("flushed between steps (256 MB write)" if self.needs_flush else
+                             f"not flushed: the step's input ({in_mb:.0f} MB f32) exceeds the 126 MB L2")
+
+    def step(self):
+        return self.net.body.forward(self.x, pooled=self.pooled, check_errors=False)
+
+    def step_e2e(self):
+        """Host images -> stem -> ternary body -> head on this rank's shard,
+        logits gathered to rank 0 (the only collective) and read back."""
+        logits = self.sharded(None)  # PipelinedResNet uploads the images chunk by chunk
+        if logits is not None:
+            self.logits_host.copy_(logits, non_blocking=True)
+        return logits
+
+    def e2e_bytes(self):
+        """(H2D, D2H) bytes per step, whole job."""
+        return self.global_batch * 3 * 224 * 224 * 4, self.global_batch * 1000 * 4
+
+    def roofline(self, flush) -> dict:
+        """Dominant kernel: the fused ternary conv (k_conv_tc, one launch per
+        conv layer, >90% of the step).  Achieved = 2 x MACs of all its launches
+        / the summed device time of those launches (CUDA events on the
+        forward's stream, L2 flushed before each forward)."""
+        ms, macs = self.net.body.conv_times(self.x, flush=flush, reps=5)
+        tot_ms = float(ms.sum())
+        per = [{"conv": i, "ms": round(float(m), 4), "gmac": round(float(a) / 1e9, 3),
+                "tops": round(2 * float(a) / (float(m) / 1e3) / 1e12, 1)} for i, (m, a) in enumerate(zip(ms, macs))]
+        return {"kernel": "fused ternary conv, tcgen05.mma kind::i8 (k_conv_tc), all conv launches of a step",
+                "bound": "tensor", "work": 2.0 * float(macs.sum()) / 1e12 / len(ms), "unit": "TFLOP/s",
+                "avg_launch_ms": tot_ms / len(ms), "launches_timed": len(ms), "per_layer": per,
+                "algorithmic": f"2 x {float(macs.sum()) / 1e9:.1f} GMAC per step over {len(ms)} launches"}
+
+    def verify(self) -> bool:
+        """Parity of the TIMED body (this batch size, persistent tile loop,
+        last partial M tile) at its first, middle and last image vs the C
+        oracle, bit-exact f32; and the e2e pipeline's bodies (its slice
+        groups) equal the timed body on the same images."""
+        import torch
+        from oracle.oracle import Oracle
+        O = Oracle()
+        pooled, out = self.net.body.forward(self.x, want_out=True)
+        idx = sorted({0, self.B // 2, self.B - 1})
+        got = out[idx].cpu().numpy()
+        del out
+        st, want = O.net_body(self.net.blocks, self.x[idx].cpu().numpy(), len(idx), 64, 56, 56)
+        ok = st == 0 and np.array_equal(got.view(np.int32), want.view(np.int32))
+        self.pipe.forward(self.images_host)
+        torch.cuda.synchronize()
+        ok = ok and torch.equal(self.pipe.pooled, pooled)
+        self.config["verified"] = {"images": idx, "oracle": "bit-exact f32 body output",
+                                   "e2e_pipeline_bodies": "pooled == timed body"}
+        return bool(ok)
+
+    def cpu_baseline(self, threads: int) -> dict:
+        from oracle.oracle import Reference
+        R = Reference()
+        h = R.net_create(self.net.blocks)
+        xs = np.ascontiguousarray(self.x[:threads].cpu().numpy())
+        runs = {}
+        for t in sorted({1, threads}):
+            rc, st = R.time_runs_net(h, xs[:t], t, 64, 56, 56, t)
+            assert rc == 0
+            runs[t] = dict(st, value=t / (st["mean_us"] / 1e6), threads=t, images=t)
+        R.net_destroy(h)
+        return cpu_baseline_line(runs, threads, "img/s",
+                                 f"{threads} images of the batch (one per host thread; 1 image for the "
+                                 f"single-thread figure), reference conv2d_ternary composition of the body")
 
 
 def build_workload(name: str, rank: int = 0, world: int = 1):
@@ -559,14 +723,13 @@ def build_workload(name: str, rank: int = 0, world: int = 1):
     if name == "conv":
         return ConvWorkload()
     if name in ("resnet18", "resnet50"):
-        from paper_2008_05101_b200.resnet import ResNetWorkload
         return ResNetWorkload(name, rank=rank, world=world)
     raise SystemExit(f"unknown workload {name}")
 
 
 def run_ours(args) -> None:
     import torch
-    rank, world, local = dist_setup()
+    rank, world, local = dist_setup(args.gpus)
     w = build_workload(args.workload, rank, world)
     assert w.verify(), "parity check failed before timing"
     # L2 between timed steps: flushed (256 MB write) unless the step's own
@@ -688,89 +851,124 @@ def run_ours(args) -> None:
 
 
 def run_reference(args) -> None:
+    """--impl reference: the reference's own CPU implementation (oracle/_ref,
+    the unmodified headers compiled from /root/reference) on every host
+    thread, same workload / metric / unit as our arm; each step is one call
+    of the reference on the workload (cfg1-3: the full input; ResNets: one
+    image per host thread).  Under torchrun only rank 0 runs it."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    from oracle.oracle import reference_lib_path
+    from oracle.oracle import Reference, host_cpu, reference_lib_path
     if reference_lib_path() is None:
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built for this host"}))
         return
+    R = Reference()
     threads = os.cpu_count() or 1
-    if args.workload in ("dot", "conv"):
-        line = reference_small(args, threads)
-    elif args.workload == "fc":
-        import numpy as np
-        rng = np.random.default_rng(0)
+    rng = np.random.default_rng(0)
+    wl = args.workload
+    if wl == "fc":
         wq = rng.integers(-1, 2, (4096, 4096)).astype(np.int8)
         rng.uniform(0.5, 1.5, 4096)
         rng.standard_normal(4096)
-        x_host = np.abs(rng.standard_normal((256, 4096))).astype(np.float32)
-        vals = []
-        cb = None
-        for i in range(args.warmup + args.steps):
-            cb = fc_reference(x_host, wq, threads, rows=64)
-            if i >= args.warmup:
-                vals.append(cb["value"])
-        v = statistics.mean(vals)
-        cb["value"] = v
-        line = {"metric": METRIC, "impl": "reference", "value": round(v, 5), "unit": "Tops/s", "n_gpus": 0,
-                "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
-                "config": {"workload": "cfg3 ternary FC 4096x4096 batch 256", "batch": 256, "in": 4096,
-                           "out": 4096},
-                "cpu_baseline": cb,
-                "e2e": {"value": round(v, 5), "unit": "Tops/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    else:
-        from paper_2008_05101_b200.resnet import reference_cpu_run
-        line = reference_cpu_run(args, METRIC, threads)
-    # the run this line stands beside: the same --gpus N launch; the reference
-    # itself computes on rank 0's host cores
-    line["n_gpus"] = args.gpus
-    line["device"] = f"host CPU, {threads} threads (rank 0 only)"
-    print(json.dumps(line), flush=True)
+        x = np.abs(rng.standard_normal((256, 4096))).astype(np.float32)
+        work, unit = 2.0 * 256 * 4096 * 4096 / 1e12, "Tops/s"
 
-
-def reference_small(args, threads) -> dict:
-    """--impl reference for cfg1 (dot) / cfg2 (conv): the reference's own CPU
-    code (oracle/_ref) on host-generated inputs of the same shape."""
-    from oracle.oracle import Reference
-    R = Reference()
-    rng = np.random.default_rng(0)
-    vals = []
-    if args.workload == "dot":
-        n, pairs = 4096, 8192
-        xs = np.abs(rng.standard_normal((pairs, n), dtype=np.float32))
-        ys = rng.standard_normal((pairs, n), dtype=np.float32)
-        xw = np.stack([R.quantize_and_pack(r, 0.5, 0.9, 1)[1] for r in xs])
-        yw = np.stack([R.quantize_and_pack(r, 0.8, 1.2, 0)[1] for r in ys])
-        wsum = DotWorkload._wsum_host(yw, n)
-        for i in range(args.warmup + args.steps):
-            st, _, sec = R.time_dot(xw, yw, n, wsum, threads)
+        def once():
+            st, r = R.time_runs_fc(x, wq, (0.5, 0.9), threads, repeats=1, warmup=0, min_run_s=0.0)
             assert st == 0
-            if i >= args.warmup:
-                vals.append(2.0 * pairs * n / sec / 1e12)
-        sample = f"{pairs} of the 65536 pairs per step, ternary_dot_nonneg over {threads} threads"
-        cfg = {"workload": "cfg1 ternary inner product N=4096 (reference CPU, oracle/_ref)", "n": n,
-               "pairs": 65536}
-    else:
+            return r["mean_us"] / 1e6
+        sample = "the full cfg3 batch (256 rows) per step: im2col_quantize_pack + packed_gemm(workers = threads)"
+        cfg = {"workload": "cfg3 ternary FC 4096x4096 batch 256", "batch": 256, "in": 4096, "out": 4096}
+    elif wl == "dot":
+        n, pairs, distinct = 4096, 65536, 8192
+        xs = np.abs(rng.standard_normal((distinct, n), dtype=np.float32))
+        ys = rng.standard_normal((distinct, n), dtype=np.float32)
+        _, xw = R.quantize_and_pack(xs.reshape(-1), 0.5, 0.9, 1)  # rows are whole words: per-row packing
+        _, yw = R.quantize_and_pack(ys.reshape(-1), 0.8, 1.2, 0)
+        # 8192 distinct pairs tiled to the 65536 of cfg1 (128 MB of operands, beyond any host cache)
+        xw = np.tile(xw.reshape(distinct, -1), (pairs // distinct, 1))
+        yw = np.tile(yw.reshape(distinct, -1), (pairs // distinct, 1))
+        del xs, ys
+        wsum = DotWorkload._wsum_host(yw, n)
+        work, unit = 2.0 * pairs * n / 1e12, "Tops/s"
+
+        def once():
+            st, r = R.time_runs_dot(xw, yw, n, wsum, threads, repeats=1, warmup=0, min_run_s=0.0)
+            assert st == 0
+            return r["mean_us"] / 1e6
+        sample = f"all {pairs} pairs per step, ternary_dot_nonneg over {threads} threads"
+        cfg = {"workload": "cfg1 ternary inner product N=4096, 65536 pairs", "n": n, "pairs": pairs}
+    elif wl == "conv":
         c, hw = 64, 56
         spec = dict(in_c=c, out_c=c, k=3, stride=1, pad=1, weights=rng.integers(-1, 2, (c, 9 * c)).astype(np.int8),
                     ta=(0.5, 0.5), tw=(1.0, 1.0), gain=rng.uniform(0.5, 1.5, c).astype(np.float32),
                     bias=rng.standard_normal(c).astype(np.float32), out_scale=1.0)
         x = np.abs(rng.standard_normal(c * hw * hw)).astype(np.float32)
-        work = 2.0 * hw * hw * 9 * c * c / 1e12
-        for i in range(args.warmup + args.steps):
-            st, _, sec = R.time_conv(x, 1, c, hw, hw, spec, threads, iters=5)
+        work, unit = 2.0 * hw * hw * 9 * c * c / 1e12, "Tops/s"
+
+        def once():
+            st, r = R.time_runs_conv(x, 1, c, hw, hw, spec, threads, repeats=1, warmup=0, min_run_s=0.0)
             assert st == 0
-            if i >= args.warmup:
-                vals.append(work / sec)
-        sample = f"5 calls of conv2d_ternary(workers={threads}) per step on the full cfg2 input"
-        cfg = {"workload": "cfg2 ternary 3x3 conv 64->64 56x56 b1 (reference CPU, oracle/_ref)"}
+            return r["mean_us"] / 1e6
+        sample = f"the full cfg2 input per step: conv2d_ternary(workers = {threads})"
+        cfg = {"workload": "cfg2 ternary 3x3 conv 64->64 56x56 b1"}
+    else:
+        from paper_2008_05101_b200.resnet import resnet_spec
+        depth = 18 if wl == "resnet18" else 50
+        blocks = resnet_spec(depth, 0)
+        h = R.net_create(blocks)
+        x = np.maximum(rng.standard_normal((threads, 64, 56, 56)), 0).astype(np.float32)
+        work, unit = float(threads), "img/s"
+
+        def once():
+            st, r = R.time_runs_net(h, x, threads, 64, 56, 56, threads, repeats=1, warmup=0, min_run_s=0.0)
+            assert st == 0
+            return r["mean_us"] / 1e6
+        gb, _ = resnet_batches(wl, max(args.gpus, 1))
+        sample = f"{threads} images per step (one per host thread) of the global batch of {gb}"
+        cfg = {"workload": f"{wl} ternary body", "model": wl, "global_batch": gb}
+    vals = []
+    for i in range(args.warmup + args.steps):
+        sec = once()
+        if i >= args.warmup:
+            vals.append(work / sec)
     v = statistics.mean(vals)
-    return {"metric": METRIC, "impl": "reference", "value": round(v, 6), "unit": "Tops/s", "n_gpus": 0,
+    cv = statistics.pstdev(vals) / v if len(vals) > 1 else 0.0
+    cfg["source"] = "reference CPU implementation (oracle/_ref, unmodified headers)"
+    line = {"metric": METRIC, "impl": "reference", "value": round(v, 6), "unit": unit, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "config": cfg,
-            "cpu_baseline": {"value": round(v, 6), "unit": "Tops/s", "cores": threads, "kind": "reference",
-                             "sample": sample},
-            "e2e": {"value": round(v, 6), "unit": "Tops/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "device": f"host CPU, {threads} threads (rank 0 only)",
+            "cpu_baseline": {"value": round(v, 6), "unit": unit, "cores": threads, "kind": "reference",
+                             "sample": sample, "cv": round(cv, 4), "host": host_cpu()},
+            "e2e": {"value": round(v, 6), "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_dry(args) -> None:
+    """--dry-run: the multi-rank plumbing without a GPU (gloo): every rank
+    computes its shard of the workload and rank 0 prints the gathered shard
+    table.  Used by the CPU tests of the --gpus N launch path."""
+    rank, world, _ = dist_setup(args.gpus, backend="gloo")
+    from paper_2008_05101_b200.shard import shard_range
+    if args.workload in ("resnet18", "resnet50"):
+        gb, scaling = resnet_batches(args.workload, world)
+        mine = shard_range(gb, rank, world)
+        mine = [mine.start, mine.count]
+    else:  # cfg1-3: independent replicas, one per rank
+        gb, scaling, mine = None, "weak", None
+    shards = [mine]
+    if world > 1:
+        import torch.distributed as dist
+        shards = [None] * world
+        dist.all_gather_object(shards, mine)
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "workload": args.workload, "n_gpus": world, "global_batch": gb,
+                          "scaling": scaling, "shards": shards,
+                          "ranks": int(os.environ.get("WORLD_SIZE", "1"))}), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
 
 
 def main():
@@ -779,11 +977,17 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default=os.environ.get("TK_BENCH_WORKLOAD", "resnet18"))
+    ap.add_argument("--workload", default=os.environ.get("TK_BENCH_WORKLOAD", "resnet18"),
+                    choices=["resnet18", "resnet50", "fc", "conv", "dot"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dry-run", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
-    if args.impl == "reference":
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(sys.argv[1:], args.gpus))
+    if args.dry_run:
+        run_dry(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)

@@ -275,6 +275,34 @@ class Oracle:
         return st, out
 
 
+class RunStats(C.Structure):
+    """ref_run_stats (oracle/ref_shim.cpp): the reference's RunStats summary."""
+    _fields_ = [("mean_us", C.c_double), ("stddev_us", C.c_double), ("median_us", C.c_double),
+                ("stable", C.c_int), ("repeats", C.c_int), ("warmup", C.c_int), ("min_run_s", C.c_double)]
+
+    def as_dict(self) -> dict:
+        return {"mean_us": self.mean_us, "stddev_us": self.stddev_us, "median_us": self.median_us,
+                "stable": bool(self.stable), "cv": self.stddev_us / self.mean_us if self.mean_us else None,
+                "repeats": self.repeats, "warmup": self.warmup, "min_run_s": self.min_run_s}
+
+
+def host_cpu() -> dict:
+    """lscpu-style record of the host the CPU baseline ran on."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    flags = _cpu_flags()
+    return {"model": model, "nproc": os.cpu_count(),
+            "avx512_vpopcntdq": "avx512_vpopcntdq" in flags, "avx512f": "avx512f" in flags,
+            "avx2": "avx2" in flags}
+
+
 def _cpu_flags() -> set[str]:
     try:
         with open("/proc/cpuinfo") as f:
@@ -336,6 +364,54 @@ class Reference:
         L.ref_time_dot.argtypes = [_u64p, _u64p, _sz, _sz, _i64p, C.c_int, C.POINTER(C.c_double), _i64p]
         L.ref_time_conv.argtypes = ([_f32p] + [C.c_int] * 4 + [C.POINTER(NdConv), C.c_int, C.c_int,
                                     C.POINTER(C.c_double), _f32p])
+
+    def make_packed_conv_layer(self, wq, in_c, out_c, kh, kw):
+        """R:linalg.hpp:118-144: (packed rows [out_c][words] u64, weight_sums i32)."""
+        wq = np.ascontiguousarray(wq, dtype=np.int8)
+        nw = words_for_lanes(in_c * kh * kw)
+        words = np.empty((out_c, nw), np.uint64)
+        sums = np.empty(out_c, np.int32)
+        f = self.lib.ref_make_packed_conv_layer
+        f.argtypes = [_i8p] + [C.c_int] * 4 + [_u64p, _i32p]
+        st = f(ptr(wq, _i8p), in_c, out_c, kh, kw, ptr(words, _u64p), ptr(sums, _i32p))
+        return st, words, sums
+
+    # ---- the reference's time_runs protocol (R:include/ternkit/bench.hpp:64-99) ----
+    def _runs(self, name, args, argtypes, repeats, warmup, min_run_s):
+        f = getattr(self.lib, name)
+        f.argtypes = argtypes + [C.c_int, C.c_int, C.c_double, C.POINTER(RunStats)]
+        st = RunStats()
+        rc = f(*args, repeats, warmup, min_run_s, C.byref(st))
+        return rc, st.as_dict()
+
+    def time_runs_net(self, handle, x, n, c, h, w, threads, repeats=5, warmup=2, min_run_s=0.6):
+        x = np.ascontiguousarray(x, np.float32)
+        return self._runs("ref_time_runs_net", [handle, ptr(x, _f32p), n, c, h, w, threads],
+                          [C.c_void_p, _f32p] + [C.c_int] * 5, repeats, warmup, min_run_s)
+
+    def time_runs_fc(self, x, wq, ta, workers, repeats=5, warmup=2, min_run_s=0.6):
+        x = np.ascontiguousarray(x, np.float32)
+        wq = np.ascontiguousarray(wq, np.int8)
+        b, k = x.shape
+        n = wq.shape[0]
+        return self._runs("ref_time_runs_fc", [ptr(x, _f32p), b, k, ptr(wq, _i8p), n, ta[0], ta[1], workers],
+                          [_f32p, C.c_int, C.c_int, _i8p, C.c_int, C.c_float, C.c_float, C.c_int],
+                          repeats, warmup, min_run_s)
+
+    def time_runs_conv(self, x, n, c, h, w, spec, workers, repeats=5, warmup=2, min_run_s=0.6):
+        keep: list = []
+        cv = make_ndconv(spec, keep)
+        x = np.ascontiguousarray(x, np.float32)
+        return self._runs("ref_time_runs_conv", [ptr(x, _f32p), n, c, h, w, C.byref(cv), workers],
+                          [_f32p] + [C.c_int] * 4 + [C.POINTER(NdConv), C.c_int], repeats, warmup, min_run_s)
+
+    def time_runs_dot(self, x, y, lanes, wsum, threads, repeats=5, warmup=2, min_run_s=0.6):
+        x = np.ascontiguousarray(x, dtype=np.uint64)
+        y = np.ascontiguousarray(y, dtype=np.uint64)
+        ws = np.ascontiguousarray(wsum, dtype=np.int64)
+        return self._runs("ref_time_runs_dot", [ptr(x, _u64p), ptr(y, _u64p), lanes, x.shape[0], ptr(ws, _i64p),
+                                                threads],
+                          [_u64p, _u64p, _sz, _sz, _i64p, C.c_int], repeats, warmup, min_run_s)
 
     def time_dot(self, x, y, lanes, wsum, threads):
         x = np.ascontiguousarray(x, dtype=np.uint64)

@@ -17,6 +17,7 @@
 #include <thread>
 #include <vector>
 
+#include "ternkit/bench.hpp"
 #include "ternkit/bitkernels.hpp"
 #include "ternkit/codec.hpp"
 #include "ternkit/linalg.hpp"
@@ -503,6 +504,119 @@ int ref_time_conv(const float* x, int n, int c, int h, int w, const nd_conv* con
     *seconds_per_call =
         std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() / iters;
     if (out) std::memcpy(out, r.data.data(), r.data.size() * 4);
+  });
+}
+
+// ---- A10: the reference's own layer build (R:linalg.hpp:118-144) ----
+// Packed weight rows ([out_c][words] u64, byte for byte) and weight sums.
+int ref_make_packed_conv_layer(const std::int8_t* wq, int in_c, int out_c, int kh, int kw,
+                               std::uint64_t* words, std::int32_t* wsums) {
+  return guard([&] {
+    const ConvGeometry g{in_c, out_c, kh, kw, 1, 0};
+    PackedConvLayer layer = make_packed_conv_layer(
+        std::span<const std::int8_t>(wq, static_cast<std::size_t>(out_c) * g.patch_len()), g,
+        {1, 1}, {1, 1}, true);
+    const std::size_t nw = words_for_lanes(g.patch_len());
+    for (int o = 0; o < out_c; ++o) {
+      std::memcpy(words + o * nw, layer.weights[o].words.data(), nw * 8);
+      wsums[o] = layer.weight_sums[o];
+    }
+  });
+}
+
+// ---- CPU-baseline protocol: the reference's own time_runs (R:bench.hpp:64-99:
+// `warmup` discarded runs, each measured run looped to >= min_run_s, mean /
+// stddev / median over `repeats`, stable = stddev <= 15% of the mean) ----
+struct ref_run_stats {
+  double mean_us, stddev_us, median_us;
+  int stable, repeats, warmup;
+  double min_run_s;
+};
+
+static void fill_stats(const RunStats& r, int repeats, int warmup, double min_run_s,
+                       ref_run_stats* st) {
+  st->mean_us = r.mean_us;
+  st->stddev_us = r.stddev_us;
+  st->median_us = r.median_us;
+  st->stable = r.stable ? 1 : 0;
+  st->repeats = repeats;
+  st->warmup = warmup;
+  st->min_run_s = min_run_s;
+}
+
+// one call = the ResNet body on n images over `threads` host threads (ref_net_run)
+int ref_time_runs_net(void* h, const float* x, int n, int c, int hh, int ww, int threads,
+                      int repeats, int warmup, double min_run_s, ref_run_stats* st) {
+  int status = kOk;
+  RunStats r = time_runs([&] {
+    int s = ref_net_run(h, x, n, c, hh, ww, threads, nullptr, nullptr);
+    if (s != kOk) status = s;
+  }, repeats, warmup, min_run_s);
+  fill_stats(r, repeats, warmup, min_run_s, st);
+  return status;
+}
+
+// one call = im2col_quantize_pack + packed_gemm(workers) of the FC (cfg3)
+int ref_time_runs_fc(const float* x, int batch, int in_c, const std::int8_t* wq, int out_c,
+                     float ta1, float ta2, int workers, int repeats, int warmup,
+                     double min_run_s, ref_run_stats* st) {
+  return guard([&] {
+    const TensorShape s{batch, in_c, 1, 1};
+    const ConvGeometry g{in_c, out_c, 1, 1, 1, 0};
+    PackedConvLayer layer = make_packed_conv_layer(
+        std::span<const std::int8_t>(wq, static_cast<std::size_t>(out_c) * in_c), g,
+        {1, 1}, {ta1, ta2}, true);
+    RunStats r = time_runs([&] {
+      Im2colBuffer buf = im2col_quantize_pack(std::span<const float>(x, s.count()), s,
+                                              {ta1, ta2}, g, QuantMode::kActivationNonneg);
+      std::vector<std::int32_t> o = packed_gemm(buf, layer, MaskMode::kOnTheFly, workers);
+    }, repeats, warmup, min_run_s);
+    fill_stats(r, repeats, warmup, min_run_s, st);
+  });
+}
+
+// one call = conv2d_ternary(workers) on the whole input (cfg2)
+int ref_time_runs_conv(const float* x, int n, int c, int h, int w, const nd_conv* conv,
+                       int workers, int repeats, int warmup, double min_run_s,
+                       ref_run_stats* st) {
+  return guard([&] {
+    PackedConvLayer layer = build_layer(*conv);
+    const TensorShape s{n, c, h, w};
+    RunStats r = time_runs([&] {
+      ConvResult o = conv2d_ternary(std::span<const float>(x, s.count()), s, layer,
+                                    MaskMode::kOnTheFly, workers);
+    }, repeats, warmup, min_run_s);
+    fill_stats(r, repeats, warmup, min_run_s, st);
+  });
+}
+
+// one call = `pairs` ternary_dot_nonneg over `threads` host threads (cfg1),
+// vectors packed once outside the timed calls
+int ref_time_runs_dot(const std::uint64_t* x, const std::uint64_t* y, std::size_t lanes,
+                      std::size_t pairs, const std::int64_t* wsum, int threads, int repeats,
+                      int warmup, double min_run_s, ref_run_stats* st) {
+  return guard([&] {
+    const std::size_t nw = words_for_lanes(lanes);
+    std::vector<PackedTernaryVector> xs(pairs), ys(pairs);
+    for (std::size_t p = 0; p < pairs; ++p) {
+      xs[p].words.assign(x + p * nw, x + (p + 1) * nw);
+      ys[p].words.assign(y + p * nw, y + (p + 1) * nw);
+      xs[p].logical_len = ys[p].logical_len = lanes;
+      xs[p].nonneg_offset = true;
+    }
+    std::vector<std::int64_t> r(pairs);
+    const int nt = threads > 0 ? threads : 1;
+    auto work = [&](int t) {
+      const std::size_t lo = pairs * t / nt, hi = pairs * (t + 1) / nt;
+      for (std::size_t p = lo; p < hi; ++p) r[p] = ternary_dot_nonneg(xs[p], ys[p], wsum[p]);
+    };
+    RunStats rs = time_runs([&] {
+      std::vector<std::thread> pool;
+      for (int t = 1; t < nt; ++t) pool.emplace_back(work, t);
+      work(0);
+      for (auto& th : pool) th.join();
+    }, repeats, warmup, min_run_s);
+    fill_stats(rs, repeats, warmup, min_run_s, st);
   });
 }
 

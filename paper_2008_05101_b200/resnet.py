@@ -15,7 +15,6 @@ from __future__ import annotations
 
 import ctypes as C
 import math
-import os
 
 import numpy as np
 import torch
@@ -40,7 +39,7 @@ def _conv(rng, in_c, out_c, k, stride, ta, relu_follows=True):
                 ta=ta, tw=(1.0, 1.0), gain=gain, bias=bias, out_scale=1.0)
 
 
-def resnet_spec(depth: int = 18, seed: int = 0, width: int = 64):
+def resnet_spec(depth: int = 18, seed: int = 0, width: int = 64, variant: str = "v1.5"):
     """Body blocks (after the stem, input width x 56 x 56) of a ResNet-depth."""
     rng = np.random.default_rng(seed)
     blocks = []
@@ -57,11 +56,15 @@ def resnet_spec(depth: int = 18, seed: int = 0, width: int = 64):
                 blocks.append(blk)
                 c = w
     elif depth == 50:
+        # v1.5 bottleneck (the stride sits on the 3x3 conv): 3.969 GMAC/img,
+        # the count SURVEY.md §8(d) uses for cfg5; variant="v1" puts it on the
+        # first 1x1 (3.738 GMAC/img)
         for stage, (w, n) in enumerate([(64, 3), (128, 4), (256, 6), (512, 3)]):
             for i in range(n):
                 s = 2 if (stage > 0 and i == 0) else 1
+                s1, s3 = (s, 1) if variant == "v1" else (1, s)
                 t1 = ta()
-                blk = dict(convs=[_conv(rng, c, w, 1, s, t1), _conv(rng, w, w, 3, 1, ta()),
+                blk = dict(convs=[_conv(rng, c, w, 1, s1, t1), _conv(rng, w, w, 3, s3, ta()),
                                   _conv(rng, w, 4 * w, 1, 1, ta(), False)])
                 if s != 1 or c != 4 * w:
                     blk["down"] = _conv(rng, c, 4 * w, 1, s, t1, False)
@@ -197,13 +200,9 @@ class TernaryResNet:
         images = images.contiguous()
         n = images.shape[0]
         y = torch.empty((n, 64, 112, 112), dtype=torch.float32, device="cuda")
-        if os.environ.get("TK_STEM") == "cudnn":
-            with torch.backends.cudnn.flags(enabled=True, allow_tf32=False):
-                y = torch.nn.functional.conv2d(images, self.stem_w, stride=2, padding=3)
-        else:
-            check(T.lib().tk_stem_conv7x7s2(tk.context(), images.data_ptr(), n, images.shape[2], images.shape[3],
-                                            self.stem_w.data_ptr(), y.data_ptr(), tk._stream()),
-                  "tk_stem_conv7x7s2")
+        check(T.lib().tk_stem_conv7x7s2(tk.context(), images.data_ptr(), n, images.shape[2], images.shape[3],
+                                        self.stem_w.data_ptr(), y.data_ptr(), tk._stream()),
+              "tk_stem_conv7x7s2")
         n, c, h, w = y.shape
         if out is None:
             out = torch.empty((n, c, (h + 1) // 2, (w + 1) // 2), dtype=torch.float32, device="cuda")
@@ -269,153 +268,3 @@ class PipelinedResNet:
             self.bodies[g].forward(self.xg[gi], pooled=self.pooled[lo:lo + g * self.cb], check_errors=False)
         self._first = False
         return self.net.head(self.pooled, out=self.logits)
-
-
-# ---------------------------------------------------------------------------
-# bench workload (cfg4 ResNet-18 b256 / cfg5 ResNet-50)
-
-class ResNetWorkload:
-    """One step = the ternary body on one batch resident in HBM (the paper's
-    protocol: first and last layers excluded); e2e = the whole network from
-    host images (pinned H2D) to logits (D2H)."""
-
-    def __init__(self, name: str = "resnet18", batch: int | None = None, seed: int = 0,
-                 rank: int = 0, world: int = 1):
-        from .shard import ShardedForward, shard_range
-        depth = 18 if name == "resnet18" else 50
-        if depth == 18:
-            # cfg4: batch 256 per GPU (weak scaling over 1/2/4/8 GPUs)
-            per_gpu = batch or int(os.environ.get("TK_BENCH_BATCH", 256))
-            global_batch, scaling = per_gpu * world, "weak"
-        else:
-            # cfg5: global batch 1024 sharded across the GPUs (strong scaling)
-            global_batch, scaling = batch or int(os.environ.get("TK_BENCH_BATCH", 1024)), "strong"
-        batch = shard_range(global_batch, rank, world).count
-        self.name, self.depth, self.B, self.global_batch = name, depth, batch, global_batch
-        self.rank, self.world, self.scaling = rank, world, scaling
-        self.net = TernaryResNet(depth, batch, seed)
-        # per-rank images: a distinct slice of the synthetic global batch
-        g = torch.Generator().manual_seed(seed + 1 + rank)
-        self.images_host = torch.rand(batch, 3, 224, 224, generator=g).pin_memory()
-        self.images_dev = self.images_host.cuda()
-        self.x = self.net.stem(self.images_dev)  # body input, resident
-        self.pooled = torch.empty((batch, self.net.body.out_shape[0]), device="cuda")
-        self.logits_host = torch.empty((global_batch if rank == 0 else 0, 1000)).pin_memory()
-        # e2e: chunked so the image upload overlaps the compute of earlier chunks
-        # (measured, tools/gpu_e2e.sh, R18 b256: 8 slices, body on 3 + 5
-        # slices 3.87 ms; on 4 + 4 3.98 ms; 4 slices, body per slice 4.24 ms)
-        if batch % 8 == 0 and batch >= 128:
-            chunks, groups = 8, [3, 5]
-        elif batch % 4 == 0 and batch >= 64:
-            chunks, groups = 4, [2, 2]
-        else:
-            chunks, groups = 1, [1]
-        chunks = int(os.environ.get("TK_E2E_CHUNKS", chunks))
-        if os.environ.get("TK_E2E_GROUPS"):
-            groups = [int(g) for g in os.environ["TK_E2E_GROUPS"].split(",")]
-        elif sum(groups) != chunks:
-            groups = None
-        self.pipe = PipelinedResNet(self.net, batch, chunks, groups)
-        self.sharded = ShardedForward(lambda _x: self.pipe.forward(self.images_host), global_batch, 1000, rank,
-                                      world)
-        self.macs_per_img = body_macs(self.net.blocks)
-        self.units_per_step = float(global_batch)  # whole job, all ranks
-        self.unit = "img/s"
-        self.launches_per_step = self.net.body.launches(False, True)
-        self.config = {"workload": f"cfg{'4' if depth == 18 else '5'} {name} ternary body, synthetic 224x224 "
-                                   f"images, global batch {global_batch} over {world} GPU(s) (paper protocol: "
-                                   f"float stem/head excluded from value, included in e2e)",
-                       "model": name, "global_batch": global_batch, "batch_per_gpu": batch, "image": 224,
-                       "parallelism": f"batch-sharded dp{world}, logits gathered to rank 0",
-                       "fused_pipeline": self.net.body.fused,
-                       "body_gmac_per_img": round(self.macs_per_img / 1e9, 4),
-                       }
-        in_mb = batch * 64 * 56 * 56 * 4 / 2**20
-        self.needs_flush = in_mb <= 126
-        self.config["l2"] = ("flushed between steps (256 MB write)" if self.needs_flush else
-                             f"not flushed: the step's input ({in_mb:.0f} MB f32) exceeds the 126 MB L2")
-
-    def step(self):
-        return self.net.body.forward(self.x, pooled=self.pooled, check_errors=False)
-
-    def step_e2e(self):
-        """Host images -> stem -> ternary body -> head on this rank's shard,
-        logits gathered to rank 0 (the only collective) and read back."""
-        logits = self.sharded(None)  # PipelinedResNet uploads the images chunk by chunk
-        if logits is not None:
-            self.logits_host.copy_(logits, non_blocking=True)
-        return logits
-
-    def e2e_bytes(self):
-        """(H2D, D2H) bytes per step, whole job."""
-        return self.global_batch * 3 * 224 * 224 * 4, self.global_batch * 1000 * 4
-
-    def roofline(self, flush) -> dict:
-        """Dominant kernel: the fused ternary conv (k_conv_tc, one launch per
-        conv layer, >90% of the step).  Achieved = 2 x MACs of all its launches
-        / the summed device time of those launches (CUDA events on the
-        forward's stream, L2 flushed before each forward)."""
-        ms, macs = self.net.body.conv_times(self.x, flush=flush, reps=5)
-        tot_ms = float(ms.sum())
-        per = [{"conv": i, "ms": round(float(m), 4), "gmac": round(float(a) / 1e9, 3),
-                "tops": round(2 * float(a) / (float(m) / 1e3) / 1e12, 1)} for i, (m, a) in enumerate(zip(ms, macs))]
-        return {"kernel": "fused ternary conv, tcgen05.mma kind::i8 (k_conv_tc), all conv launches of a step",
-                "bound": "tensor", "work": 2.0 * float(macs.sum()) / 1e12 / len(ms), "unit": "TFLOP/s",
-                "avg_launch_ms": tot_ms / len(ms), "launches_timed": len(ms), "per_layer": per,
-                "algorithmic": f"2 x {float(macs.sum()) / 1e9:.1f} GMAC per step over {len(ms)} launches"}
-
-    def verify(self) -> bool:
-        """Body parity on a 2-image subsample vs the C oracle (bit-exact f32)."""
-        from oracle.oracle import Oracle
-        O = Oracle()
-        sub = 2
-        xb = self.x[:sub].contiguous()
-        body2 = TernaryBody(self.net.blocks, sub, 64, 56, 56)
-        _, out = body2.forward(xb, want_out=True)
-        st, want = O.net_body(self.net.blocks, xb.cpu().numpy(), sub, 64, 56, 56)
-        return st == 0 and np.array_equal(out.cpu().numpy().view(np.int32), want.view(np.int32))
-
-    def cpu_baseline(self, threads: int) -> dict:
-        from oracle.oracle import Reference
-        R = Reference()
-        n = threads
-        xs = np.ascontiguousarray(self.x[:n].cpu().numpy())
-        h = R.net_create(self.net.blocks)
-        st, _, sec = R.net_run(h, xs, n, 64, 56, 56, threads)
-        R.net_destroy(h)
-        assert st == 0
-        return {"value": n / sec, "unit": "img/s", "cores": threads, "kind": "reference",
-                "sample": f"{n} images of the batch, one per host thread, reference conv2d_ternary "
-                          f"composition (oracle/_ref, unmodified headers)", "seconds": sec}
-
-
-def reference_cpu_run(args, metric: str, threads: int) -> dict:
-    """bench.py --impl reference for the ResNet workloads: the reference's own
-    CPU implementation (oracle/_ref) of the ternary body, all host threads,
-    each step a bounded sample of `threads` images."""
-    import statistics
-    from oracle.oracle import Reference
-    depth = 18 if args.workload == "resnet18" else 50
-    blocks = resnet_spec(depth, 0)
-    R = Reference()
-    h = R.net_create(blocks)
-    rng = np.random.default_rng(1)
-    n = threads
-    x = np.maximum(rng.standard_normal((n, 64, 56, 56)), 0).astype(np.float32)
-    vals = []
-    for i in range(args.warmup + args.steps):
-        st, _, sec = R.net_run(h, x, n, 64, 56, 56, threads)
-        assert st == 0
-        if i >= args.warmup:
-            vals.append(n / sec)
-    R.net_destroy(h)
-    v = statistics.mean(vals)
-    batch = 256 if depth == 18 else 128
-    cb = {"value": round(v, 4), "unit": "img/s", "cores": threads, "kind": "reference",
-          "sample": f"{n} images per step (one per host thread) of the batch-{batch} workload"}
-    return {"metric": metric, "impl": "reference", "value": round(v, 4), "unit": "img/s", "n_gpus": 0,
-            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
-            "config": {"workload": f"{args.workload} ternary body (reference CPU, oracle/_ref)",
-                       "model": args.workload, "batch_per_gpu": batch},
-            "cpu_baseline": cb,
-            "e2e": {"value": round(v, 4), "unit": "img/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}

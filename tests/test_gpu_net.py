@@ -89,6 +89,36 @@ def test_resnet50_body_subsample(oracle):
     _check(oracle, blocks, x, 1, 64, 56, 56, expect_fused=True)
 
 
+def _full_batch_samples(oracle, depth, batch, images, seed):
+    """The body exactly as the bench times it (one TernaryBody over the whole
+    batch: persistent tile loop, late work items, the last partial M tile and
+    the pad ring), sampled at the first, a middle and the last image."""
+    from paper_2008_05101_b200.resnet import TernaryBody, resnet_spec
+    blocks = resnet_spec(depth, seed=0)
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    x = torch.randn((batch, 64, 56, 56), generator=g, device="cuda").relu_()
+    body = TernaryBody(blocks, batch, 64, 56, 56)
+    assert body.fused
+    _, out = body.forward(x, want_out=True)
+    got = out[images].cpu().numpy()
+    del out
+    xs = x[images].cpu().numpy()
+    st, want = oracle.net_body(blocks, xs, len(images), 64, 56, 56)
+    assert st == 0
+    mism = np.count_nonzero(got.view(np.int32) != want.view(np.int32))
+    assert mism == 0, f"{mism} of {got.size} body outputs differ"
+
+
+def test_resnet18_full_batch_samples(oracle):
+    """cfg4 at its timed batch (256): images 0, 127, 255 vs the oracle."""
+    _full_batch_samples(oracle, 18, 256, [0, 127, 255], seed=11)
+
+
+def test_resnet50_full_batch_samples(oracle):
+    """cfg5 at its timed batch (1024 on one GPU): images 0, 511, 1023 vs the oracle."""
+    _full_batch_samples(oracle, 50, 1024, [0, 511, 1023], seed=12)
+
+
 def test_batch_independence_large_batch():
     """Images are independent: image i of a batch-64 run equals a batch-1 run."""
     from paper_2008_05101_b200.resnet import resnet_spec
