@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.environ.get("TK_LIB_PATH") or os.path.join(HERE, "libternkit_b200.so")  # override: A/B experiments
+LIB_PATH = os.path.join(HERE, "libternkit_b200.so")
 
 TK_OK = 0
 TK_ERR_INVALID = 1

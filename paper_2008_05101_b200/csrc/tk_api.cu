@@ -5,6 +5,9 @@
 #include <string.h>
 
 #include <algorithm>
+#include <map>
+#include <mutex>
+#include <utility>
 #include <vector>
 
 #include "tk_internal.cuh"
@@ -83,6 +86,19 @@ void* tk_workspace(tk_context* ctx, size_t bytes) {
   return ctx->ws;
 }
 
+cudaError_t tk_smem_attr(const void* kernel, int bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> done;  // (kernel, device) -> bytes set
+  int dev = 0;
+  if (const cudaError_t e = cudaGetDevice(&dev); e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  int& have = done[{kernel, dev}];
+  if (have >= bytes) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) have = bytes;
+  return e;
+}
+
 extern "C" {
 
 int tk_version(void) { return 100; }
@@ -144,6 +160,7 @@ int tk_context_create(int device, tk_context** out) {
 }
 
 int tk_context_destroy(tk_context* ctx) {
+  TK_ON_DEVICE(ctx);
   if (!ctx) return TK_OK;
   cudaDeviceSynchronize();
   if (ctx->ws) cudaFree(ctx->ws);
@@ -154,6 +171,7 @@ int tk_context_destroy(tk_context* ctx) {
 }
 
 int tk_context_sync(tk_context* ctx, void* stream) {
+  TK_ON_DEVICE(ctx);
   if (!ctx) return TK_ERR_INVALID;
   cudaStream_t s = (cudaStream_t)stream;
   unsigned long long* h = (unsigned long long*)ctx->pinned;
@@ -166,6 +184,7 @@ int tk_context_sync(tk_context* ctx, void* stream) {
 
 int tk_pack(tk_context* ctx, const int8_t* values, size_t n, uint64_t* words,
             void* stream) {
+  TK_ON_DEVICE(ctx);
   if (!ctx || (n && (!values || !words))) return TK_ERR_INVALID;
   TK_CUDA(tk_launch_pack_int8(values, n, words, ctx->d_err, (cudaStream_t)stream));
   return TK_OK;
@@ -173,6 +192,7 @@ int tk_pack(tk_context* ctx, const int8_t* values, size_t n, uint64_t* words,
 
 int tk_unpack(tk_context* ctx, const uint64_t* words, size_t n, int8_t* values,
               void* stream) {
+  TK_ON_DEVICE(ctx);
   if (!ctx || (n && (!values || !words))) return TK_ERR_INVALID;
   TK_CUDA(tk_launch_unpack(words, n, values, (cudaStream_t)stream));
   return TK_OK;
@@ -181,6 +201,7 @@ int tk_unpack(tk_context* ctx, const uint64_t* words, size_t n, int8_t* values,
 int tk_quantize_pack(tk_context* ctx, const float* x, size_t rows, size_t n,
                      float a1, float a2, int mode, uint64_t* words,
                      void* stream) {
+  TK_ON_DEVICE(ctx);
   if (!ctx) return TK_ERR_INVALID;
   tk_qparams q;
   const int st = tk_make_qparams(a1, a2, mode, &q);  // R:quantizer.hpp:63
@@ -194,6 +215,7 @@ int tk_quantize_pack(tk_context* ctx, const float* x, size_t rows, size_t n,
 int tk_ternary_dot_batched(tk_context* ctx, const uint64_t* x,
                            const uint64_t* y, size_t words, size_t pairs,
                            const int64_t* wsum, int64_t* out, void* stream) {
+  TK_ON_DEVICE(ctx);
   if (!ctx || (pairs && (!x || !y || !out))) return TK_ERR_INVALID;
   TK_CUDA(tk_launch_dot_batched(x, y, words, pairs, wsum, out,
                                 (cudaStream_t)stream));
@@ -211,6 +233,7 @@ int tk_im2col_quantize_pack(tk_context* ctx, const float* x, int n, int c,
                             int h, int w, int kh, int kw, int stride, int pad,
                             float a1, float a2, int mode, uint64_t* rows,
                             void* stream) {
+  TK_ON_DEVICE(ctx);
   if (!ctx) return TK_ERR_INVALID;
   if (!geom_ok(c, h, w, kh, kw, stride, pad) || n < 0 || h < 0 || w < 0)
     return TK_ERR_INVALID;  // geom.validate before t.validate, R:linalg.hpp:178-179
@@ -229,6 +252,7 @@ int tk_layer_create(tk_context* ctx, const int8_t* weights_host, int in_c,
                     float tw2, float ta1, float ta2, int activation_nonneg,
                     const float* gain_host, const float* bias_host,
                     float out_scale, tk_layer** out) {
+  TK_ON_DEVICE(ctx);
   if (!ctx || !out) return TK_ERR_INVALID;
   if (in_c <= 0 || out_c <= 0 || kh <= 0 || kw <= 0 || stride <= 0 || pad < 0)
     return TK_ERR_INVALID;
@@ -316,6 +340,7 @@ int tk_layer_create(tk_context* ctx, const int8_t* weights_host, int in_c,
 }
 
 int tk_layer_destroy(tk_layer* L) {
+  TK_ON_DEVICE(L ? L->ctx : nullptr);
   if (!L) return TK_OK;
   cudaDeviceSynchronize();
   cudaFree(L->d_words); cudaFree(L->d_mask); cudaFree(L->d_wsum);
@@ -378,6 +403,7 @@ int tk_layer_words_host(const tk_layer* L, uint64_t* words_host,
 int tk_packed_gemm(tk_context* ctx, const tk_layer* L, const uint64_t* rows,
                    size_t row_count, size_t row_len, int nonneg_offset,
                    int mask_mode, int32_t* out, void* stream) {
+  TK_ON_DEVICE(ctx);
   if (!ctx || !L) return TK_ERR_INVALID;
   if (row_len != (size_t)L->K) return TK_ERR_INVALID;
   if (mask_mode == TK_MASK_PRECOMPUTED && !L->masks_ready) return TK_ERR_MASKS;
@@ -404,6 +430,7 @@ int tk_packed_gemm(tk_context* ctx, const tk_layer* L, const uint64_t* rows,
 int tk_conv2d_ternary(tk_context* ctx, const tk_layer* L, const float* x,
                       int n, int h, int w, int mask_mode, float* out,
                       void* stream) {
+  TK_ON_DEVICE(ctx);
   if (!ctx || !L) return TK_ERR_INVALID;
   if (!geom_ok(L->in_c, h, w, L->kh, L->kw, L->stride, L->pad) || n < 0)
     return TK_ERR_INVALID;
@@ -470,21 +497,25 @@ int quantize_levels(tk_context* ctx, const float* x, int rows, int n, float a1, 
 
 int tk_gemm_levels(tk_context* ctx, const tk_layer* L, const int8_t* a_s8, int m_rows,
                    int out_mode, void* out, void* stream) {
+  TK_ON_DEVICE(ctx);
   return gemm_levels(ctx, L, a_s8, m_rows, out_mode, out, false, stream);
 }
 
 int tk_gemm_levels_fp4(tk_context* ctx, const tk_layer* L, const uint8_t* a_fp4, int m_rows, int out_mode,
                        void* out, void* stream) {
+  TK_ON_DEVICE(ctx);
   return gemm_levels(ctx, L, (const int8_t*)a_fp4, m_rows, out_mode, out, true, stream);
 }
 
 int tk_quantize_levels(tk_context* ctx, const float* x, int rows, int n, float a1, float a2,
                        int mode, int k_pad, int8_t* out, void* stream) {
+  TK_ON_DEVICE(ctx);
   return quantize_levels(ctx, x, rows, n, a1, a2, mode, k_pad, false, out, stream);
 }
 
 int tk_quantize_levels_fp4(tk_context* ctx, const float* x, int rows, int n, float a1, float a2, int mode,
                            int k_pad, uint8_t* out, void* stream) {
+  TK_ON_DEVICE(ctx);
   return quantize_levels(ctx, x, rows, n, a1, a2, mode, k_pad, true, (int8_t*)out, stream);
 }
 
@@ -492,6 +523,7 @@ int tk_quantize_levels_fp4(tk_context* ctx, const float* x, int rows, int n, flo
 int tk_fully_connected_ternary(tk_context* ctx, const tk_layer* L,
                                const float* x, int batch, int mask_mode,
                                float* out, void* stream) {
+  TK_ON_DEVICE(ctx);
   if (!ctx || !L) return TK_ERR_INVALID;
   if (L->kh != 1 || L->kw != 1 || L->pad != 0) return TK_ERR_INVALID;
   if (batch < 0) return TK_ERR_INVALID;

@@ -87,6 +87,7 @@ unsigned grid_of(size_t work, unsigned per) {
 extern "C" {
 
 int tk_pack_binary(tk_context* ctx, const int8_t* values, size_t n, uint64_t* words, void* stream) {
+  TK_ON_DEVICE(ctx);
   if (!ctx || (n && (!values || !words))) return TK_ERR_INVALID;
   const size_t nwords = (n + 63) / 64;
   if (nwords == 0) return TK_OK;
@@ -96,6 +97,7 @@ int tk_pack_binary(tk_context* ctx, const int8_t* values, size_t n, uint64_t* wo
 
 int tk_binary_dot_batched(tk_context* ctx, const uint64_t* x, const uint64_t* y, size_t words, size_t logical_len,
                           size_t pairs, int64_t* out, void* stream) {
+  TK_ON_DEVICE(ctx);
   if (!ctx || (pairs && (!x || !y || !out)) || logical_len > words * 64) return TK_ERR_INVALID;
   if (pairs == 0) return TK_OK;
   k_binary_dot_batched<<<grid_of(pairs, 8), 256, 0, (cudaStream_t)stream>>>(x, y, words, logical_len, pairs, out);
@@ -105,6 +107,7 @@ int tk_binary_dot_batched(tk_context* ctx, const uint64_t* x, const uint64_t* y,
 int tk_multibit_dot_batched(tk_context* ctx, const uint64_t* x_planes, int m, const uint64_t* y_planes, int k,
                             const double* x_scales, const double* y_scales, size_t words, size_t logical_len,
                             size_t pairs, double* out, void* stream) {
+  TK_ON_DEVICE(ctx);
   if (!ctx || m <= 0 || k <= 0 || logical_len > words * 64) return TK_ERR_INVALID;  // R:bitkernels.hpp:199-203
   if (pairs && (!x_planes || !y_planes || !x_scales || !y_scales || !out)) return TK_ERR_INVALID;
   if (pairs == 0) return TK_OK;

@@ -12,6 +12,26 @@
 
 #include "../../include/ternkit_b200.h"
 
+// Experiment / profiling overrides (kernel phase knobs, tile-shape forcing,
+// in-kernel timestamps).  Compiled in only with -DTK_PROFILE, for the A/B
+// builds of tools/; the production library reads no environment variables
+// and its kernels carry no profiling branches (TK_DBG(x) folds to 0).
+#ifdef TK_PROFILE
+#include <stdlib.h>
+inline int tk_knob(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v ? atoi(v) : dflt;
+}
+#define TK_DBG(x) (x)
+#else
+inline constexpr int tk_knob(const char*, int dflt) { return dflt; }
+#define TK_DBG(x) 0
+#endif
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is per device: raise it
+// once per (kernel, current device), thread-safe (tk_api.cu).
+cudaError_t tk_smem_attr(const void* kernel, int bytes);
+
 #define TK_KAUXI32 0x55555555u
 
 struct tk_context {
@@ -22,6 +42,22 @@ struct tk_context {
   size_t ws_bytes = 0;
   void* pinned = nullptr;               // 8-byte host slot for the error word
 };
+
+// Every C-ABI entry that takes a context runs on the context's device and
+// leaves the caller's current device as it found it.
+struct tk_device_guard {
+  int prev = -1, dev = -1;
+  explicit tk_device_guard(const tk_context* c) {
+    if (c && cudaGetDevice(&prev) == cudaSuccess && prev != c->device && cudaSetDevice(c->device) == cudaSuccess)
+      dev = c->device;
+  }
+  ~tk_device_guard() {
+    if (dev >= 0) cudaSetDevice(prev);
+  }
+  tk_device_guard(const tk_device_guard&) = delete;
+  tk_device_guard& operator=(const tk_device_guard&) = delete;
+};
+#define TK_ON_DEVICE(ctx) const tk_device_guard tk_device_guard_(ctx)
 
 struct tk_layer {
   tk_context* ctx = nullptr;

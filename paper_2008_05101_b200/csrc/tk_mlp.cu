@@ -67,6 +67,7 @@ extern "C" {
 
 int tk_matmul_t(tk_context* ctx, const float* x, const float* w, const float* bias, int batch, int in_dim,
                 int out_dim, int relu, float* y, void* stream) {
+  TK_ON_DEVICE(ctx);
   if (!ctx || !x || !w || !y || batch < 0 || in_dim <= 0 || out_dim <= 0) return TK_ERR_INVALID;
   const long long total = (long long)batch * out_dim;
   if (total == 0) return TK_OK;
@@ -78,6 +79,7 @@ int tk_matmul_t(tk_context* ctx, const float* x, const float* w, const float* bi
 
 int tk_residual_relu_rows(tk_context* ctx, float* z, const float* h, long long count, int hidden,
                           const float* cal_gain, const float* cal_bias, void* stream) {
+  TK_ON_DEVICE(ctx);
   if (!ctx || !z || !h || count < 0 || hidden <= 0 || count % hidden) return TK_ERR_INVALID;
   if ((cal_gain == nullptr) != (cal_bias == nullptr)) return TK_ERR_INVALID;
   if (count == 0) return TK_OK;

@@ -181,7 +181,7 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
   __shared__ int s_ph[4];
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const bool stamp = (p.dbg & 16) && blockIdx.x < 148;
+  const bool stamp = (TK_DBG(p.dbg) & 16) && blockIdx.x < 148;
   if (stamp && threadIdx.x == 0) g_stamps[blockIdx.x * 8 + 0] = gtime();
 
   if (threadIdx.x == 0) {
@@ -243,7 +243,7 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
         if (lane == 0) {
           if (stamp && blockIdx.x == 0 && h_round * p.hs + hs_i < 32)
             g_trace[0 * 32 + h_round * p.hs + hs_i] = clock64();
-          if (p.dbg & 2) {
+          if (TK_DBG(p.dbg) & 2) {
             sm100::mbar_arrive(&h_full[hs_i]);
           } else {
             sm100::mbar_arrive_expect_tx(&h_full[hs_i], (uint32_t)(p.n_ph * p.nbox * p.hbox * R));
@@ -288,7 +288,7 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
     uint32_t toff[KT];
 #pragma unroll
     for (int t = 0; t < KT; ++t) toff[t] = (uint32_t)(p.tap_slot[t] * p.HB + p.tap_shift[t] * R);
-    const bool do_mma = !(p.dbg & 1);
+    const bool do_mma = !(TK_DBG(p.dbg) & 1);
     int hs_i = 0, h_round = 0, ws_i = 0, w_round = 0, acc = 0, a_round = 0, it = 0;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
       if (stamp && lane == 0 && blockIdx.x == 0 && it < 32) g_trace[6 * 32 + it] = clock64();
@@ -375,7 +375,7 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
     sm100::pdl_wait();  // skip inputs / outputs of the neighbouring layers
     const uint32_t* ep = eparam;
     const uint32_t ostride = (uint32_t)oplane;  // CH channel planes < 2^31 elements
-    const bool has_skip = (p.skip || (BN >= 128 && p.skip16)) && !(p.dbg & (4 | 512));
+    const bool has_skip = (p.skip || (BN >= 128 && p.skip16)) && !(TK_DBG(p.dbg) & (4 | 512));
     // element offset of (item's first channel, this thread's position) in the
     // NCHW skip tensor, or -1 when the position is past the batch / padding
     auto skip_at = [&](int item) -> long long {
@@ -409,8 +409,8 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
       const int mt = mi * MT + grp % MT;
       const uint32_t tcol = (uint32_t)(it % kAcc) * (BN * MT) + (grp % MT) * BN;
       const int acc = it % kAcc;
-      if (p.dbg & 8) {  // profiling: bare accumulator hand-off
-        if (!(p.dbg & 64) || lane == 0) sm100::mbar_wait(&a_full[acc], (it / kAcc) & 1);
+      if (TK_DBG(p.dbg) & 8) {  // profiling: bare accumulator hand-off
+        if (!(TK_DBG(p.dbg) & 64) || lane == 0) sm100::mbar_wait(&a_full[acc], (it / kAcc) & 1);
         __syncwarp();
         if (stamp && blockIdx.x == 0 && it < 32 && qtr == 0 && lane == 0) g_trace[3 * 32 + it] = clock64();
         sm100::tc_fence_after();
@@ -446,7 +446,7 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
 #pragma unroll
         for (int j = 0; j < CH; ++j, off += ostride) sk[j] = __ldg(p.skip + skb + off);
       }
-      if (p.dbg & 1024)
+      if (TK_DBG(p.dbg) & 1024)
         sm100::mbar_wait(&a_full[acc], (it / kAcc) & 1);
       else
         sm100::mbar_wait_sleep(&a_full[acc], (it / kAcc) & 1, 2000);
@@ -459,7 +459,7 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
         else
           sm100::tmem_ld16(tmem + ((uint32_t)(qtr * 32) << 16) + tcol + c0, r);
         sm100::tmem_ld_wait();
-        if (!valid || (p.dbg & 4)) continue;
+        if (!valid || (TK_DBG(p.dbg) & 4)) continue;
         const int n0 = nt * BN + c0;
         if (p.ithr) {
           // integer-threshold epilogue: level = (s*acc > c0) + (s*acc > c1)
@@ -590,13 +590,13 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
 #pragma unroll
           for (int j = 0; j < CH; ++j) v[j] = v[j] < 0.0f ? 0.0f : v[j];  // std::max(v, 0.0f)
         }
-        if (p.fout && !(p.dbg & 256)) {
+        if (p.fout && !(TK_DBG(p.dbg) & 256)) {
           float* ob = p.fout + fbase + (long long)n0 * oplane;
           uint32_t off = 0;
 #pragma unroll
           for (int j = 0; j < CH; ++j, off += ostride) ob[off] = v[j];
         }
-        if (p.n_q > 0 && !(p.dbg & 128)) {
+        if (p.n_q > 0 && !(TK_DBG(p.dbg) & 128)) {
           // quantizer input checks (R:quantizer.hpp:37-41,53-55), once per
           // value: after the ReLU a value is >= 0 (or -0.0) unless NaN
           bool bad = false;
@@ -990,11 +990,7 @@ void pool_nchw(const float* x, int NC, int HW, float* out, cudaStream_t s) {
   // planes per block: up to 64, within 96 KB of staged floats
   const int planes = std::max(1, std::min(64, (96 * 1024) / (HW * 4)));
   const size_t smem = (size_t)planes * HW * 4;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_pool_nchw, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024 + 4096);
-    attr = true;
-  }
+  tk_smem_attr((const void*)k_pool_nchw, 96 * 1024 + 4096);
   k_pool_nchw<<<(NC + planes - 1) / planes, planes, smem, s>>>(x, NC, HW, out);
 }
 
@@ -1082,8 +1078,7 @@ struct Conv {
 // (|acc| <= 2 * in_c * k * k); env TK_NET_F32_RESIDUAL=1 keeps f32 (A/B)
 bool s16_ok(const Conv& cv) { return 2 * cv.d.in_c * cv.d.k * cv.d.k < 32768; }
 bool f32_residual_forced() {
-  static const bool f = getenv("TK_NET_F32_RESIDUAL") && atoi(getenv("TK_NET_F32_RESIDUAL"));
-  return f;
+  return tk_knob("TK_NET_F32_RESIDUAL", 0) != 0;
 }
 
 }  // namespace
@@ -1192,7 +1187,7 @@ int prepare_conv_weights(Conv& cv, int R) {
   cv.R = R;
   cv.chunks = chunks;
   cv.BN = d.out_c >= 256 ? 256 : d.out_c;  // 64, 128, 256
-  if (getenv("TK_CONV_BNMAX")) cv.BN = std::min(cv.BN, std::max(64, atoi(getenv("TK_CONV_BNMAX"))));
+  if (const int bnmax = tk_knob("TK_CONV_BNMAX", 0)) cv.BN = std::min(cv.BN, std::max(64, bnmax));
   cv.n_tiles = d.out_c / cv.BN;
   const size_t blk = (size_t)cv.BN * R;
   std::vector<int8_t> w((size_t)cv.n_tiles * chunks * taps * blk, 0);
@@ -1371,7 +1366,7 @@ int setup_fused(tk_net* net) {
       // (MT > 1 kernels carry the integer epilogue only)
       // (MT = 4 measured no faster than 2 on the ResNet-18 stage-1 convs)
       cv.MT = (cv.BN == 64 && inner && k.m_tiles > 1) ? 2 : 1;
-      if (getenv("TK_CONV_MT")) cv.MT = std::min(cv.MT, std::max(1, atoi(getenv("TK_CONV_MT"))));
+      if (const int mt = tk_knob("TK_CONV_MT", 0)) cv.MT = std::min(cv.MT, std::max(1, mt));
       k.m_items = (k.m_tiles + cv.MT - 1) / cv.MT;
       {
         const int span = k.halo_rows;
@@ -1392,7 +1387,7 @@ int setup_fused(tk_net* net) {
       const int wmin = k.resident ? wbytes_all : 3 * k.WB;
       // halo ring depth: enough stages in flight to cover the TMA latency
       // (env TK_CONV_HS caps it for experiments)
-      const int hs_cap = getenv("TK_CONV_HS") ? std::max(1, atoi(getenv("TK_CONV_HS"))) : 8;
+      const int hs_cap = std::max(1, tk_knob("TK_CONV_HS", 8));
       k.hs = std::max(1, std::min(hs_cap, (budget - wmin) / halo_stage));
       k.ws = k.resident ? 1 : std::max(2, std::min(8, (budget - k.hs * halo_stage) / k.WB));
       const int wregion = k.resident ? wbytes_all : k.ws * k.WB;
@@ -1414,7 +1409,7 @@ int setup_fused(tk_net* net) {
       // (the s16 residual path is compiled into the BN >= 128 kernels only)
       auto s16_pair = [&](const Conv& dv) {
         return !f32_residual_forced() && s16_ok(dv) && dv.d.out_c >= 128 && cvs.back().d.out_c >= 128 &&
-               !getenv("TK_CONV_BNMAX");
+               !tk_knob("TK_CONV_BNMAX", 0);
       };
       if (cv.is_down && s16_pair(cv)) {  // (its f32 tensor holds the s16 values)
         k.aout = reinterpret_cast<int16_t*>(k.fout);
@@ -1470,7 +1465,7 @@ int setup_fused(tk_net* net) {
             pack16 = thr[((size_t)o * 3 + 2) * N + n] == 1 && c0 >= -32768 && c0 <= 32767 && c1 >= -32768 &&
                      c1 <= 32767;
           }
-        if (getenv("TK_CONV_NOPACK16")) pack16 = false;  // experiments
+        if (tk_knob("TK_CONV_NOPACK16", 0)) pack16 = false;
         k.ithr16 = pack16 ? 1 : 0;
         if (pack16) {
           std::vector<int> p16((size_t)k.n_q * N);
@@ -1486,14 +1481,14 @@ int setup_fused(tk_net* net) {
       }
       if (cv.MT > 1 && !k.ithr) return TK_ERR_UNSUPPORTED;  // (inner predicate above mirrors this)
       k.err = net->ctx->d_err;
-      k.dbg = getenv("TK_CONV_DBG") ? atoi(getenv("TK_CONV_DBG")) : 0;
+      k.dbg = tk_knob("TK_CONV_DBG", 0);
       // profiling: TK_CONV_DBG_ONLY=<launch order index> limits the knob to one conv
-      if (getenv("TK_CONV_DBG_ONLY") && atoi(getenv("TK_CONV_DBG_ONLY")) != conv_no) k.dbg = 0;
+      if (tk_knob("TK_CONV_DBG_ONLY", -1) >= 0 && tk_knob("TK_CONV_DBG_ONLY", -1) != conv_no) k.dbg = 0;
       if (!map_rows(&cv.in_map, in.p, (unsigned long long)(in.C / in.R) * in.phases * in.pos, in.R, k.hbox))
         return TK_ERR_CUDA;
       const int items = k.m_items * k.n_tiles;
       cv.grid = std::min(items, net->ctx->num_sms);
-      if (getenv("TK_CONV_GRID")) cv.grid = std::min(items, atoi(getenv("TK_CONV_GRID")));  // profiling
+      if (const int g = tk_knob("TK_CONV_GRID", 0)) cv.grid = std::min(items, g);
     }
   // input packing
   PackIn& pk = net->pack;
@@ -1517,12 +1512,9 @@ int setup_fused(tk_net* net) {
 
 template <int BN, int R, int KT, int MT>
 cudaError_t launch_conv(const Conv& cv, const float* x, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    // 227 KB per block, less the kernel's static shared tables
-    cudaFuncSetAttribute(k_conv_tc<BN, R, KT, MT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024);
-    attr = true;
-  }
+  // 227 KB per block, less the kernel's static shared tables
+  if (const cudaError_t e = tk_smem_attr((const void*)k_conv_tc<BN, R, KT, MT>, 226 * 1024); e != cudaSuccess)
+    return e;
   ConvK k = cv.k;
   if (cv.skip_f == -2) k.skip = x;  // identity shortcut = the forward's input
   // programmatic dependent launch (env TK_PDL=1): the prologue (TMEM,
@@ -1536,7 +1528,7 @@ cudaError_t launch_conv(const Conv& cv, const float* x, cudaStream_t s) {
   cfg.stream = s;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  static const int pdl = getenv("TK_PDL") ? atoi(getenv("TK_PDL")) : 0;
+  const int pdl = tk_knob("TK_PDL", 0);
   at[0].val.programmaticStreamSerializationAllowed = pdl;
   cfg.attrs = at;
   cfg.numAttrs = 1;
@@ -1612,6 +1604,7 @@ extern "C" {
 
 int tk_net_create(tk_context* ctx, const tk_block_desc* blocks, int n_blocks, int batch, int in_c, int in_h,
                   int in_w, int mode, tk_net** out) {
+  TK_ON_DEVICE(ctx);
   if (!ctx || !blocks || n_blocks <= 0 || batch <= 0 || !out) return TK_ERR_INVALID;
   tk_net* net = new tk_net;
   net->ctx = ctx;
@@ -1652,6 +1645,7 @@ int tk_net_create(tk_context* ctx, const tk_block_desc* blocks, int n_blocks, in
 
 int tk_affine_relu_maxpool(tk_context* ctx, const float* x, int n, int c, int h, int w, const float* gain,
                            const float* bias, float* out, void* stream) {
+  TK_ON_DEVICE(ctx);
   if (!ctx || !x || !gain || !bias || !out || n < 0 || c <= 0 || h <= 0 || w <= 0) return TK_ERR_INVALID;
   const int ho = (h + 1) / 2, wo = (w + 1) / 2;
   const long long total = (long long)n * c * ho * wo;
@@ -1669,35 +1663,23 @@ int tk_affine_relu_maxpool(tk_context* ctx, const float* x, int n, int c, int h,
 
 int tk_stem_conv7x7s2(tk_context* ctx, const float* images, int n, int h, int w, const float* weights,
                       float* out, void* stream) {
+  TK_ON_DEVICE(ctx);
   if (!ctx || !images || !weights || !out || n < 0 || h <= 0 || w <= 0) return TK_ERR_INVALID;
   const int ho = (h + 6 - 7) / 2 + 1, wo = (w + 6 - 7) / 2 + 1;
   if (wo > kStemCols || (w + 6) > kStemInCols) return TK_ERR_UNSUPPORTED;  // one CTA spans the width
   if (n == 0) return TK_OK;
   const int smem = (147 * 64 + 2 * 3 * kStemInRows * 2 * kStemPitch) * 4;
-  // variant (A/B knob TK_STEM_VARIANT): 1 = 8 channels x FFMA2 (512 threads,
-  // the default: fastest measured), 0 = 16 x FFMA2 (256), 2 = 16 x FFMA
-  // (256), 3 = 8 x FFMA (512)
-  static const int variant = getenv("TK_STEM_VARIANT") ? atoi(getenv("TK_STEM_VARIANT")) : 1;
-  auto go = [&](auto kern, int threads) {
-    static bool attr[4] = {false, false, false, false};
-    if (!attr[variant & 3]) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      attr[variant & 3] = true;
-    }
-    const int items = n * ((ho + kStemRows - 1) / kStemRows);
-    kern<<<std::min(items, ctx->num_sms), threads, smem, (cudaStream_t)stream>>>(images, weights, n, h, w, ho, wo,
-                                                                                 out);
-  };
-  switch (variant & 3) {
-    case 1: go(k_stem_conv<8, true>, 512); break;
-    case 2: go(k_stem_conv<16, false>, 256); break;
-    case 3: go(k_stem_conv<8, false>, 512); break;
-    default: go(k_stem_conv<16, true>, 256); break;
-  }
+  // 8 channels x packed FFMA2 per thread, 512 threads (the fastest of the
+  // 8/16-channel, FFMA/FFMA2 variants measured)
+  if (tk_smem_attr((const void*)k_stem_conv<8, true>, smem) != cudaSuccess) return TK_ERR_CUDA;
+  const int items = n * ((ho + kStemRows - 1) / kStemRows);
+  k_stem_conv<8, true><<<std::min(items, ctx->num_sms), 512, smem, (cudaStream_t)stream>>>(images, weights, n, h, w,
+                                                                                        ho, wo, out);
   return cudaGetLastError() == cudaSuccess ? TK_OK : TK_ERR_CUDA;
 }
 
 int tk_net_destroy(tk_net* net) {
+  TK_ON_DEVICE(net ? net->ctx : nullptr);
   if (!net) return TK_OK;
   cudaDeviceSynchronize();
   for (auto& cvs : net->convs)
@@ -1785,14 +1767,14 @@ int tk_net_conv_times(tk_net* net, float* ms, double* macs) {
 }
 
 int tk_net_forward(tk_context* ctx, tk_net* net, const float* x, float* out, float* pooled, void* stream) {
+  TK_ON_DEVICE(ctx);
   if (!ctx || !net || !x) return TK_ERR_INVALID;
   cudaStream_t s = (cudaStream_t)stream;
   if (net->fused) {
     PackIn pk = net->pack;
     pk.x = x;
     const long long rows = (long long)pk.N * pk.H * pk.W;
-    static const bool old_pack = getenv("TK_PACK_INPUT_OLD") != nullptr;  // A/B
-    if (rows < (1ll << 31) && !old_pack) {
+    if (rows < (1ll << 31)) {
       k_pack_input_rows<<<(unsigned)std::min<long long>((rows + 255) / 256, 148 * 16), 256, 0, s>>>(pk);
     } else {
       const long long total = rows * (pk.C / 16);
@@ -1804,7 +1786,7 @@ int tk_net_forward(tk_context* ctx, tk_net* net, const float* x, float* out, flo
       for (const auto& cv : cvs) {
         if (net->timing) cudaEventRecord(net->ev[2 * ci], s);
         if (const cudaError_t ce = run_conv(cv, x, s); ce != cudaSuccess) {
-          if (getenv("TK_NET_DEBUG")) fprintf(stderr, "tk_net_forward: conv %d: %s\n", ci, cudaGetErrorString(ce));
+          if (tk_knob("TK_NET_DEBUG", 0)) fprintf(stderr, "tk_net_forward: conv %d: %s\n", ci, cudaGetErrorString(ce));
           return TK_ERR_CUDA;
         }
         if (net->timing) cudaEventRecord(net->ev[2 * ci + 1], s);

@@ -81,7 +81,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 k_gemm_tc_i8(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
              const __grid_constant__ CUtensorMap tmO, int direct, int mcx,
              int M, int N, int num_kb, int m_pad, int n_pad, int S, tk_epilogue e,
-             int dbg) {
+             int dbg_arg) {
+  const int dbg = TK_DBG(dbg_arg);  // profiling phase knobs: 0 in the production build
   constexpr int kStages = TcSmem<BN>::kStages;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (sm100::smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -592,7 +593,7 @@ cudaError_t launch(const int8_t* a, int M, int num_kb, const tk_layer* L, tk_epi
   const int m_pad = (M + BM - 1) / BM * BM;
   // K-block-major [kb][rows][128 B]: a 2-D map of num_kb*rows rows of 128 bytes
   // A multicast across a (mcx, 1, 1) cluster of N tiles (direct path only)
-  static const int mc_env = getenv("TK_GEMM_MC") ? atoi(getenv("TK_GEMM_MC")) : 0;  // profiling override
+  const int mc_env = tk_knob("TK_GEMM_MC", 0);
   const int n_tiles = (L->out_c + BN - 1) / BN;
   int mcx = 1;
   if (direct == 1) {
@@ -609,11 +610,8 @@ cudaError_t launch(const int8_t* a, int M, int num_kb, const tk_layer* L, tk_epi
     if (!make_map(&ta, a, (uint64_t)num_kb * m_pad, 128, BM / mcx)) return cudaErrorInvalidValue;
     if (!make_map(&tb, F4 ? L->d_w4 : L->d_w8, (uint64_t)num_kb * L->n_pad, 128, BN)) return cudaErrorInvalidValue;
   }
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(k_gemm_tc_i8<BN, F4>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcSmem<BN>::kBytes);
-    attr_set = true;
-  }
+  if (const cudaError_t er = tk_smem_attr((const void*)k_gemm_tc_i8<BN, F4>, TcSmem<BN>::kBytes); er != cudaSuccess)
+    return er;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((L->out_c + BN - 1) / BN, (M + BM - 1) / BM, S);
   cfg.blockDim = dim3(kThreads, 1, 1);
@@ -624,15 +622,19 @@ cudaError_t launch(const int8_t* a, int M, int num_kb, const tk_layer* L, tk_epi
   at[0].val.clusterDim.x = mcx;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = S;
-  // programmatic dependent launch (TK_GEMM_PDL=0 disables, for A/B)
-  static const int pdl = getenv("TK_GEMM_PDL") ? atoi(getenv("TK_GEMM_PDL")) : 1;
+  // programmatic dependent launch
+  const int pdl = tk_knob("TK_GEMM_PDL", 1);
   at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[1].val.programmaticStreamSerializationAllowed = pdl;
   cfg.attrs = at;
   cfg.numAttrs = 2;
-  static const int dbg0 = getenv("TK_GEMM_DBG") ? atoi(getenv("TK_GEMM_DBG")) : 0;  // profiling knob
+#ifdef TK_PROFILE
   static int launches = 0;
+  const int dbg0 = tk_knob("TK_GEMM_DBG", 0);
   const int dbg = (dbg0 & 16) ? (dbg0 | ((launches++ & 1) << 8)) : dbg0;  // stamp buffer parity
+#else
+  const int dbg = 0;
+#endif
   return cudaLaunchKernelEx(&cfg, k_gemm_tc_i8<BN, F4>, ta, tb, to, direct, mcx, M, L->out_c, num_kb, m_pad, L->n_pad, S, e,
                             dbg);
 }
@@ -659,7 +661,7 @@ cudaError_t tk_launch_gemm_tc_fmt(const int8_t* a_s8, int M, int k_pad, const tk
   const long tiles_m = (M + BM - 1) / BM;
   const int N = L->out_c, num_kb = fp4 ? k_pad / 256 : k_pad / BK;
   const int max_kb = fp4 ? kMaxKbPerCta / 2 : kMaxKbPerCta;  // 256 levels per fp4 K block
-  static const bool no_direct = getenv("TK_GEMM_NODIRECT") != nullptr;  // profiling A/B
+  const bool no_direct = tk_knob("TK_GEMM_NODIRECT", 0) != 0;
   const bool row_major = !no_direct && e.mode != TK_EPI_F32_NCHW && N % 4 == 0 && (uintptr_t)e.out % 16 == 0;
   auto tiles_of = [&](int bn) { return tiles_m * ((N + bn - 1) / bn); };
   // Tile shape: the operand traffic from L2 into the SMs,
@@ -675,10 +677,10 @@ cudaError_t tk_launch_gemm_tc_fmt(const int8_t* a_s8, int M, int k_pad, const tk
     BN = N > 64 ? 128 : 64;
     while (2 * S <= 4 && 2 * S <= num_kb && tiles_of(BN) * 2 * S <= 148) S *= 2;
   }
-  if (getenv("TK_GEMM_BN")) BN = std::max(64, std::min(256, atoi(getenv("TK_GEMM_BN"))));  // profiling
-  if (getenv("TK_GEMM_SPLIT")) {  // profiling override
+  if (const int bn = tk_knob("TK_GEMM_BN", 0)) BN = std::max(64, std::min(256, bn));
+  if (const int sp = tk_knob("TK_GEMM_SPLIT", 0)) {
     S = 1;
-    while (2 * S <= std::min({8, num_kb, atoi(getenv("TK_GEMM_SPLIT"))})) S *= 2;
+    while (2 * S <= std::min({8, num_kb, sp})) S *= 2;
   }
   // s16 partials (cluster exchange, or the NCHW staging) stay exact; the
   // direct S == 1 epilogue reads the 32-bit accumulators straight from TMEM

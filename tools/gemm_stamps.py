@@ -5,6 +5,8 @@ import os
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+import _profile  # noqa: E402,F401  (the -DTK_PROFILE build: experiment knobs)
 os.environ["TK_GEMM_DBG"] = str(16 | int(os.environ.get("DBG", "0")))
 
 import numpy as np  # noqa: E402
