@@ -56,6 +56,11 @@ extern "C" {
 #define TK_BACKEND_TC_I8 2   /* tcgen05.mma kind::i8 tensor cores             */
 #define TK_BACKEND_TC_F4 3   /* tcgen05.mma kind::mxf4 (E2M1 levels, unit E8M0
                                 block scales: exact, 2x the i8 MMA rate)       */
+#define TK_BACKEND_TC_CONV 4 /* conv2d_ternary: implicit-im2col fused conv
+                                (quantize into padded channel-last s8 planes,
+                                then tcgen05 kind::i8 over the 3x3 taps with
+                                the folded-BN NCHW epilogue); other entries
+                                and ineligible shapes use the kind::i8 GEMM */
 
 typedef struct tk_context tk_context;
 typedef struct tk_layer tk_layer;
@@ -102,6 +107,12 @@ int tk_quantize_pack(tk_context* ctx, const float* x, size_t rows, size_t n,
 int tk_ternary_dot_batched(tk_context* ctx, const uint64_t* x,
                            const uint64_t* y, size_t words, size_t pairs,
                            const int64_t* wsum, int64_t* out, void* stream);
+/* detail::ternary_dot_words_premask / ternary_dot_premask: the same with the
+ * zero seeds supplied, seeds: [pairs][words] u64 (make_zero_seeds of y, or any
+ * caller buffer -- the TM of R:bitkernels.hpp:66-72 uses them as given).
+ *                                                    R:bitkernels.hpp:87-97,130-149 */
+int tk_ternary_dot_premask_batched(tk_context* ctx, const uint64_t* x, const uint64_t* y, const uint64_t* seeds,
+                                   size_t words, size_t pairs, const int64_t* wsum, int64_t* out, void* stream);
 
 /* ---- linalg (R:linalg.hpp) ---------------------------------------------- */
 /* im2col_quantize_pack(x NCHW, shape, thr, geom, mode)  R:linalg.hpp:173-225

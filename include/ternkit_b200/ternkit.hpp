@@ -180,6 +180,37 @@ inline std::uint64_t ternary_multiply_word(std::uint64_t xw, std::uint64_t yw) n
   return (~(xw ^ yw) | d) & ~(d << 1);
 }
 
+// R:bitkernels.hpp:66-72: the zero seed supplied by the caller
+inline std::uint64_t ternary_multiply_word_premask(std::uint64_t xw, std::uint64_t yw, std::uint64_t d) noexcept {
+  return (~(xw ^ yw) | d) & ~(d << 1);
+}
+
+namespace detail {
+
+// R:bitkernels.hpp:76-85 (the reference's raw-pointer entry), on the GPU:
+// host words in, sum popcount(TM) - 32 * words out.  Like the reference it
+// does not throw; a CUDA failure terminates (there is no CPU fallback).
+inline std::int64_t ternary_dot_words(const std::uint64_t* x, const std::uint64_t* y, std::size_t words) noexcept {
+  b200::DevBuf<std::uint64_t> xd(x, words), yd(y, words);
+  b200::DevBuf<std::int64_t> o(1);
+  b200::check(tk_ternary_dot_batched(b200::ctx(), xd.p, yd.p, words, 1, nullptr, o.p, nullptr), "ternary_dot_words");
+  b200::sync("ternary_dot_words");
+  return o.host(1)[0];
+}
+
+// R:bitkernels.hpp:87-97: the same with the zero seeds supplied (used as given)
+inline std::int64_t ternary_dot_words_premask(const std::uint64_t* x, const std::uint64_t* y,
+                                              const std::uint64_t* seed, std::size_t words) noexcept {
+  b200::DevBuf<std::uint64_t> xd(x, words), yd(y, words), sd(seed, words);
+  b200::DevBuf<std::int64_t> o(1);
+  b200::check(tk_ternary_dot_premask_batched(b200::ctx(), xd.p, yd.p, sd.p, words, 1, nullptr, o.p, nullptr),
+              "ternary_dot_words_premask");
+  b200::sync("ternary_dot_words_premask");
+  return o.host(1)[0];
+}
+
+}  // namespace detail
+
 inline std::int64_t ternary_dot(const PackedTernaryVector& x, const PackedTernaryVector& y) {
   if (x.logical_len != y.logical_len) throw std::invalid_argument("ternary_dot: length mismatch");
   const std::size_t nw = x.words.size();
@@ -200,7 +231,13 @@ inline std::int64_t ternary_dot_premask(const PackedTernaryVector& x, const Pack
                                         std::span<const std::uint64_t> seeds) {
   if (x.logical_len != y.logical_len) throw std::invalid_argument("ternary_dot_premask: length mismatch");
   if (seeds.size() != y.words.size()) throw std::invalid_argument("ternary_dot_premask: seed buffer mismatch");
-  return ternary_dot(x, y);
+  const std::size_t nw = x.words.size();
+  b200::DevBuf<std::uint64_t> xd(x.words.data(), nw), yd(y.words.data(), nw), sd(seeds.data(), nw);
+  b200::DevBuf<std::int64_t> o(1);
+  b200::check(tk_ternary_dot_premask_batched(b200::ctx(), xd.p, yd.p, sd.p, nw, 1, nullptr, o.p, nullptr),
+              "ternary_dot_premask");
+  b200::sync("ternary_dot_premask");
+  return o.host(1)[0];
 }
 
 inline std::int64_t ternary_dot_nonneg(const PackedTernaryVector& a, const PackedTernaryVector& w,

@@ -31,6 +31,7 @@ TK_BACKEND_AUTO = 0
 TK_BACKEND_POPC = 1
 TK_BACKEND_TC_I8 = 2
 TK_BACKEND_TC_F4 = 3
+TK_BACKEND_TC_CONV = 4
 
 _vp = C.c_void_p
 _sz = C.c_size_t
@@ -50,6 +51,7 @@ SIGNATURES = {
     "tk_unpack": (_i, [_vp, _vp, _sz, _vp, _vp]),
     "tk_quantize_pack": (_i, [_vp, _vp, _sz, _sz, _f, _f, _i, _vp, _vp]),
     "tk_ternary_dot_batched": (_i, [_vp, _vp, _vp, _sz, _sz, _vp, _vp, _vp]),
+    "tk_ternary_dot_premask_batched": (_i, [_vp, _vp, _vp, _vp, _sz, _sz, _vp, _vp, _vp]),
     "tk_im2col_quantize_pack": (_i, [_vp, _vp] + [_i] * 8 + [_f, _f, _i, _vp, _vp]),
     "tk_layer_create": (_i, [_vp, _vp] + [_i] * 6 + [_f] * 4 + [_i, _vp, _vp, _f, C.POINTER(_vp)]),
     "tk_layer_destroy": (_i, [_vp]),

@@ -217,8 +217,15 @@ int tk_ternary_dot_batched(tk_context* ctx, const uint64_t* x,
                            const int64_t* wsum, int64_t* out, void* stream) {
   TK_ON_DEVICE(ctx);
   if (!ctx || (pairs && (!x || !y || !out))) return TK_ERR_INVALID;
-  TK_CUDA(tk_launch_dot_batched(x, y, words, pairs, wsum, out,
-                                (cudaStream_t)stream));
+  TK_CUDA(tk_launch_dot_batched(x, y, nullptr, words, pairs, wsum, out, (cudaStream_t)stream));
+  return TK_OK;
+}
+
+int tk_ternary_dot_premask_batched(tk_context* ctx, const uint64_t* x, const uint64_t* y, const uint64_t* seeds,
+                                   size_t words, size_t pairs, const int64_t* wsum, int64_t* out, void* stream) {
+  TK_ON_DEVICE(ctx);
+  if (!ctx || (pairs && (!x || !y || !seeds || !out))) return TK_ERR_INVALID;
+  TK_CUDA(tk_launch_dot_batched(x, y, seeds, words, pairs, wsum, out, (cudaStream_t)stream));
   return TK_OK;
 }
 
@@ -329,8 +336,12 @@ int tk_layer_create(tk_context* ctx, const int8_t* weights_host, int in_c,
   }
   L->h_words = (uint64_t*)malloc(words.size() * 8);
   L->h_wsum = (int32_t*)malloc(out_c * 4);
+  L->h_gain = (float*)malloc(out_c * 4);
+  L->h_bias = (float*)malloc(out_c * 4);
   memcpy(L->h_words, words.data(), words.size() * 8);
   memcpy(L->h_wsum, wsum.data(), out_c * 4);
+  memcpy(L->h_gain, gain.data(), out_c * 4);
+  memcpy(L->h_bias, bias.data(), out_c * 4);
   if (!ok) {
     tk_layer_destroy(L);
     return TK_ERR_CUDA;
@@ -343,12 +354,15 @@ int tk_layer_destroy(tk_layer* L) {
   TK_ON_DEVICE(L ? L->ctx : nullptr);
   if (!L) return TK_OK;
   cudaDeviceSynchronize();
+  tk_fconv_destroy_plans(L);
   cudaFree(L->d_words); cudaFree(L->d_mask); cudaFree(L->d_wsum);
   cudaFree(L->d_zcnt); cudaFree(L->d_gain); cudaFree(L->d_bias);
   cudaFree(L->d_w8);
   cudaFree(L->d_w4);
   free(L->h_words);
   free(L->h_wsum);
+  free(L->h_gain);
+  free(L->h_bias);
   delete L;
   return TK_OK;
 }
@@ -360,7 +374,7 @@ int tk_layer_precompute_masks(tk_layer* L) {
 }
 
 int tk_layer_set_backend(tk_layer* L, int backend) {
-  if (!L || backend < TK_BACKEND_AUTO || backend > TK_BACKEND_TC_F4)
+  if (!L || backend < TK_BACKEND_AUTO || backend > TK_BACKEND_TC_CONV)
     return TK_ERR_INVALID;
   L->backend = backend;
   return TK_OK;
@@ -372,6 +386,8 @@ int tk_layer_set_backend(tk_layer* L, int backend) {
 // beat s8.
 int tk_layer_get_backend(const tk_layer* L, int m_rows) {
   if (!L) return TK_ERR_INVALID;
+  // (TC_CONV is a conv2d_ternary kernel; everywhere else it is the kind::i8 GEMM)
+  if (L->backend == TK_BACKEND_TC_CONV) return TK_BACKEND_TC_I8;
   if (L->backend != TK_BACKEND_AUTO) return L->backend;
   if (!(tk_tc_supported(m_rows, L->out_c, L->k_pad) && m_rows >= 128)) return TK_BACKEND_POPC;
   // FP4 unless its coarser K blocks (256 levels) leave too few K blocks to
@@ -444,6 +460,11 @@ int tk_conv2d_ternary(tk_context* ctx, const tk_layer* L, const float* x,
   const size_t M = (size_t)n * oh * ow;
   if (M == 0) return TK_OK;
   cudaStream_t s = (cudaStream_t)stream;
+  // nonneg activations on a tensor-core-shaped conv: the fused implicit-im2col
+  // kernel (quantize into padded channel-last planes, 9 tap MMAs per tile, the
+  // NCHW epilogue in the same kernel)
+  if ((L->backend == TK_BACKEND_AUTO || L->backend == TK_BACKEND_TC_CONV) && tk_fconv_eligible(L, n, h, w))
+    return tk_fconv_run(L, x, n, h, w, out, s);
   tk_epilogue e{TK_EPI_F32_NCHW, oh * ow, L->d_gain, L->d_bias, L->out_scale, out};
   const int be = tk_layer_get_backend(L, (int)M);
   const size_t rows_bytes = M * L->wpr64 * 8;

@@ -10,6 +10,10 @@
 #include <stdint.h>
 #include <stddef.h>
 
+#include <map>
+#include <mutex>
+#include <tuple>
+
 #include "../../include/ternkit_b200.h"
 
 // Experiment / profiling overrides (kernel phase knobs, tile-shape forcing,
@@ -82,7 +86,19 @@ struct tk_layer {
   // host mirrors (PackedConvLayer::weights / weight_sums)
   uint64_t* h_words = nullptr;
   int32_t* h_wsum = nullptr;
+  float* h_gain = nullptr;  // [out_c] folded affine (host copy for conv plans)
+  float* h_bias = nullptr;
+  // conv2d_ternary plans of the fused implicit-im2col kernel, per input shape
+  // (n, h, w), built on first use (tk_net.cu)
+  mutable std::mutex plan_mu;
+  mutable std::map<std::tuple<int, int, int>, tk_net*> plans;
 };
+
+// conv2d_ternary through the fused implicit-im2col tensor-core conv
+// (tk_net.cu): eligibility of a layer / input shape, the run, plan cleanup
+bool tk_fconv_eligible(const tk_layer* L, int n, int h, int w);
+int tk_fconv_run(const tk_layer* L, const float* x, int n, int h, int w, float* out, cudaStream_t s);
+void tk_fconv_destroy_plans(tk_layer* L);
 
 // Float thresholds that reproduce the reference quantizer exactly:
 // lane code = (p > t0) | (p > t1) << 1.  `lo_ok` is the smallest valid input
@@ -145,10 +161,9 @@ cudaError_t tk_launch_quantize_levels(const float* x, size_t rows, size_t n, tk_
                                       int8_t* out, unsigned long long* err, cudaStream_t s);
 
 // launchers (tk_popc.cu)
-cudaError_t tk_launch_dot_batched(const uint64_t* x, const uint64_t* y,
-                                  size_t words, size_t pairs,
-                                  const int64_t* wsum, int64_t* out,
-                                  cudaStream_t s);
+// seed: optional [pairs][words] zero seeds (premask form), else derived from y
+cudaError_t tk_launch_dot_batched(const uint64_t* x, const uint64_t* y, const uint64_t* seed, size_t words,
+                                  size_t pairs, const int64_t* wsum, int64_t* out, cudaStream_t s);
 // epilogue modes of the GEMM kernels
 enum { TK_EPI_I32 = 0, TK_EPI_F32_NCHW = 1, TK_EPI_F32_ROWS = 2 };
 struct tk_epilogue {

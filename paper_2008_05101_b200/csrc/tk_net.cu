@@ -660,9 +660,29 @@ struct PackIn {
   long long q_pos[2];
   int Hp, Wp, PH, PW;
   unsigned long long* err;
+  // error positions: 0 = NCHW element order (network input); 1 = the
+  // im2col evaluation order of conv2d_ternary (R:linalg.hpp:173-225) for a
+  // kk x kk / stride ks / pad kpad conv with OH x OW outputs
+  int ek, kk, ks, kpad, OH, OW;
 };
 
+// Error key of input element (n, c, y, x).  In im2col order it is
+// row * K + lane of the element's FIRST use (its smallest output row, then
+// the tap within that row), so the minimum over bad elements is the error
+// the reference throws first; -1 when no patch reads the element.
+__device__ __forceinline__ long long pack_err_key(const PackIn& p, int n, int c, int y, int x) {
+  if (!p.ek) return (((long long)n * p.C + c) * p.H + y) * p.W + x;
+  int oy = y + p.kpad - (p.kk - 1), ox = x + p.kpad - (p.kk - 1);
+  oy = oy <= 0 ? 0 : (oy + p.ks - 1) / p.ks;
+  ox = ox <= 0 ? 0 : (ox + p.ks - 1) / p.ks;
+  const int ky = y + p.kpad - oy * p.ks, kx = x + p.kpad - ox * p.ks;
+  if (ky < 0 || kx < 0 || oy >= p.OH || ox >= p.OW) return -1;
+  const long long row = ((long long)n * p.OH + oy) * p.OW + ox;
+  return row * (p.kk * p.kk * p.C) + (ky * p.kk + kx) * p.C + c;
+}
+
 __global__ void k_pack_input(const PackIn p) {
+  sm100::pdl_launch_dependents();  // a PDL-launched conv may start its prologue
   const long long HW = (long long)p.H * p.W;
   const int groups = p.C / 16;
   const long long total = (long long)p.N * groups * HW;
@@ -684,7 +704,10 @@ __global__ void k_pack_input(const PackIn p) {
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         const int e = tk_error_code(v[j], 1);
-        if (e != TK_OK) tk_raise(p.err, (unsigned long long)(((long long)n * p.C + g * 16 + j) * HW + pix), e);
+        if (e != TK_OK) {
+          const long long key = pack_err_key(p, n, g * 16 + j, y, xx);
+          if (key >= 0) tk_raise(p.err, (unsigned long long)key, e);
+        }
       }
     }
     const int py = y + 1, px = xx + 1;
@@ -718,6 +741,7 @@ __global__ void k_pack_input(const PackIn p) {
 // whole by one thread (full 32-byte sectors instead of 16-byte pieces from
 // four different warps).
 __global__ void __launch_bounds__(256) k_pack_input_rows(const PackIn p) {
+  sm100::pdl_launch_dependents();
   const int HW = p.H * p.W;
   const int total = p.N * HW;
   const int groups = p.C / 16;
@@ -742,7 +766,10 @@ __global__ void __launch_bounds__(256) k_pack_input_rows(const PackIn p) {
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
           const int e = tk_error_code(v[j], 1);
-          if (e != TK_OK) tk_raise(p.err, (unsigned long long)(((long long)n * p.C + g * 16 + j) * HW + pix), e);
+          if (e != TK_OK) {
+            const long long key = pack_err_key(p, n, g * 16 + j, y, xx);
+            if (key >= 0) tk_raise(p.err, (unsigned long long)key, e);
+          }
         }
       }
       for (int o = 0; o < p.n_q; ++o) {
@@ -1086,6 +1113,7 @@ bool f32_residual_forced() {
 struct tk_net {
   tk_context* ctx = nullptr;
   int fused = 0;
+  int single = 0;  // one conv, no residual (conv2d_ternary plan, tk_fconv_run)
   int batch = 0, in_c = 0, in_h = 0, in_w = 0;
   int out_c = 0, out_h = 0, out_w = 0;
   std::vector<tk_block_desc> blocks;
@@ -1113,6 +1141,9 @@ bool fused_ok(const tk_net* net) {
     int h = H, w = W, c = C;
     auto ok = [&](const tk_conv_desc& d, int hh, int ww, int cc) {
       if (d.in_c != cc || d.out_c % 64 || d.in_c % 64) return false;
+      // channel chunks of R = 64 (C == 64) or 128, N tiles of 64 / 128 / 256
+      if (!(d.in_c == 64 || d.in_c % 128 == 0) || !(d.out_c == 64 || d.out_c == 128 || d.out_c % 256 == 0))
+        return false;
       if (!((d.k == 3 && d.pad == 1) || (d.k == 1 && d.pad == 0))) return false;
       if (d.stride != 1 && d.stride != 2) return false;
       if (d.stride == 2 && ((hh % 2) || (ww % 2))) return false;
@@ -1260,6 +1291,8 @@ int want_f32(tk_net* net, int C, int H, int W) {
   return (int)net->f32.size() - 1;
 }
 
+int finish_fused(tk_net* net, int pack_a, int pack_b);
+
 int setup_fused(tk_net* net) {
   int H = net->in_h, W = net->in_w, C = net->in_c;
   const int nb = (int)net->blocks.size();
@@ -1331,6 +1364,13 @@ int setup_fused(tk_net* net) {
     }
     H = h; W = w; C = c;
   }
+  return finish_fused(net, bin[0].idx_conv1, bin[0].idx_down != bin[0].idx_conv1 ? bin[0].idx_down : -1);
+}
+
+// Allocation, per-conv kernel parameters and the input packing of a wired
+// fused plan (net->convs); pack_a / pack_b: the s8 tensors the input is
+// quantized into (pack_b may be -1).
+int finish_fused(tk_net* net, int pack_a, int pack_b) {
   // allocate tensors
   for (auto& t : net->s8) {
     if (cudaMalloc(&t.p, t.bytes()) != cudaSuccess) return TK_ERR_CUDA;
@@ -1493,10 +1533,10 @@ int setup_fused(tk_net* net) {
   // input packing
   PackIn& pk = net->pack;
   pk.N = net->batch; pk.C = net->in_c; pk.H = net->in_h; pk.W = net->in_w;
-  const S8T& s0 = net->s8[bin[0].idx_conv1];
+  const S8T& s0 = net->s8[pack_a];
   pk.Hp = s0.Hp; pk.Wp = s0.Wp; pk.PH = s0.Hp / 2; pk.PW = s0.Wp / 2;
   pk.n_q = 0;
-  int ids[2] = {bin[0].idx_conv1, bin[0].idx_down != bin[0].idx_conv1 ? bin[0].idx_down : -1};
+  int ids[2] = {pack_a, pack_b};
   for (int id : ids) {
     if (id < 0) continue;
     const S8T& q = net->s8[id];
@@ -1511,16 +1551,17 @@ int setup_fused(tk_net* net) {
 }
 
 template <int BN, int R, int KT, int MT>
-cudaError_t launch_conv(const Conv& cv, const float* x, cudaStream_t s) {
+cudaError_t launch_conv(const Conv& cv, const float* x, float* out, int pdl, cudaStream_t s) {
   // 227 KB per block, less the kernel's static shared tables
   if (const cudaError_t e = tk_smem_attr((const void*)k_conv_tc<BN, R, KT, MT>, 226 * 1024); e != cudaSuccess)
     return e;
   ConvK k = cv.k;
   if (cv.skip_f == -2) k.skip = x;  // identity shortcut = the forward's input
-  // programmatic dependent launch (env TK_PDL=1): the prologue (TMEM,
-  // barriers, resident weights) may overlap the previous kernel's tail.  Off
-  // by default: with one persistent CTA per SM no SM frees early enough for
-  // it to pay off (measured: tools/bench_pdl.sh)
+  if (cv.out_f == -3) k.fout = out;  // the caller's output (conv2d_ternary plans)
+  // programmatic dependent launch: the prologue (TMEM, barriers, resident
+  // weights) may overlap the previous kernel's tail.  Off inside the network:
+  // with one persistent CTA per SM no SM frees early enough for it to pay
+  // off (measured); on for conv2d_ternary plans, behind the input packing.
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(cv.grid);
   cfg.blockDim = dim3(conv_threads(BN, MT));
@@ -1528,7 +1569,6 @@ cudaError_t launch_conv(const Conv& cv, const float* x, cudaStream_t s) {
   cfg.stream = s;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  const int pdl = tk_knob("TK_PDL", 0);
   at[0].val.programmaticStreamSerializationAllowed = pdl;
   cfg.attrs = at;
   cfg.numAttrs = 1;
@@ -1536,28 +1576,45 @@ cudaError_t launch_conv(const Conv& cv, const float* x, cudaStream_t s) {
 }
 
 template <int BN, int R, int KT>
-cudaError_t launch_conv_mt(const Conv& cv, const float* x, cudaStream_t s) {
+cudaError_t launch_conv_mt(const Conv& cv, const float* x, float* out, int pdl, cudaStream_t s) {
   if constexpr (BN == 64) {
-    if (cv.MT == 4) return launch_conv<BN, R, KT, 4>(cv, x, s);
-    if (cv.MT == 2) return launch_conv<BN, R, KT, 2>(cv, x, s);
+    if (cv.MT == 4) return launch_conv<BN, R, KT, 4>(cv, x, out, pdl, s);
+    if (cv.MT == 2) return launch_conv<BN, R, KT, 2>(cv, x, out, pdl, s);
   }
-  return launch_conv<BN, R, KT, 1>(cv, x, s);
+  return launch_conv<BN, R, KT, 1>(cv, x, out, pdl, s);
 }
 
 template <int KT>
-cudaError_t run_conv_kt(const Conv& cv, const float* x, cudaStream_t s) {
+cudaError_t run_conv_kt(const Conv& cv, const float* x, float* out, int pdl, cudaStream_t s) {
   if (cv.R == 64) {
-    if (cv.BN == 64) return launch_conv_mt<64, 64, KT>(cv, x, s);
-    if (cv.BN == 128) return launch_conv_mt<128, 64, KT>(cv, x, s);
-    return launch_conv_mt<256, 64, KT>(cv, x, s);
+    if (cv.BN == 64) return launch_conv_mt<64, 64, KT>(cv, x, out, pdl, s);
+    if (cv.BN == 128) return launch_conv_mt<128, 64, KT>(cv, x, out, pdl, s);
+    return launch_conv_mt<256, 64, KT>(cv, x, out, pdl, s);
   }
-  if (cv.BN == 64) return launch_conv_mt<64, 128, KT>(cv, x, s);
-  if (cv.BN == 128) return launch_conv_mt<128, 128, KT>(cv, x, s);
-  return launch_conv_mt<256, 128, KT>(cv, x, s);
+  if (cv.BN == 64) return launch_conv_mt<64, 128, KT>(cv, x, out, pdl, s);
+  if (cv.BN == 128) return launch_conv_mt<128, 128, KT>(cv, x, out, pdl, s);
+  return launch_conv_mt<256, 128, KT>(cv, x, out, pdl, s);
 }
 
-cudaError_t run_conv(const Conv& cv, const float* x, cudaStream_t s) {
-  return cv.k.n_taps == 9 ? run_conv_kt<9>(cv, x, s) : run_conv_kt<1>(cv, x, s);
+// x: the forward's input (identity shortcut of the first block); out: the
+// caller's output buffer of a conv2d_ternary plan (out_f == -3)
+cudaError_t run_conv(const Conv& cv, const float* x, float* out, int pdl, cudaStream_t s) {
+  return cv.k.n_taps == 9 ? run_conv_kt<9>(cv, x, out, pdl, s) : run_conv_kt<1>(cv, x, out, pdl, s);
+}
+
+// input packing: a thread per position walking all channels for large
+// inputs (whole R-byte rows per thread); a thread per (position, 16-channel
+// group) when the input is too small to fill the SMs that way
+cudaError_t launch_pack(PackIn pk, const float* x, cudaStream_t s) {
+  pk.x = x;
+  const long long rows = (long long)pk.N * pk.H * pk.W;
+  if (rows < (1ll << 31) && rows >= 148ll * 256 * 2) {
+    k_pack_input_rows<<<(unsigned)std::min<long long>((rows + 255) / 256, 148 * 16), 256, 0, s>>>(pk);
+  } else {
+    const long long total = rows * (pk.C / 16);
+    k_pack_input<<<(unsigned)std::min<long long>((total + 255) / 256, 148 * 64), 256, 0, s>>>(pk);
+  }
+  return cudaGetLastError();
 }
 
 int setup_generic(tk_net* net) {
@@ -1771,21 +1828,12 @@ int tk_net_forward(tk_context* ctx, tk_net* net, const float* x, float* out, flo
   if (!ctx || !net || !x) return TK_ERR_INVALID;
   cudaStream_t s = (cudaStream_t)stream;
   if (net->fused) {
-    PackIn pk = net->pack;
-    pk.x = x;
-    const long long rows = (long long)pk.N * pk.H * pk.W;
-    if (rows < (1ll << 31)) {
-      k_pack_input_rows<<<(unsigned)std::min<long long>((rows + 255) / 256, 148 * 16), 256, 0, s>>>(pk);
-    } else {
-      const long long total = rows * (pk.C / 16);
-      k_pack_input<<<(unsigned)std::min<long long>((total + 255) / 256, 148 * 64), 256, 0, s>>>(pk);
-    }
-    if (cudaGetLastError() != cudaSuccess) return TK_ERR_CUDA;
+    if (launch_pack(net->pack, x, s) != cudaSuccess) return TK_ERR_CUDA;
     int ci = 0;
     for (const auto& cvs : net->convs)
       for (const auto& cv : cvs) {
         if (net->timing) cudaEventRecord(net->ev[2 * ci], s);
-        if (const cudaError_t ce = run_conv(cv, x, s); ce != cudaSuccess) {
+        if (const cudaError_t ce = run_conv(cv, x, nullptr, tk_knob("TK_PDL", 0), s); ce != cudaSuccess) {
           if (tk_knob("TK_NET_DEBUG", 0)) fprintf(stderr, "tk_net_forward: conv %d: %s\n", ci, cudaGetErrorString(ce));
           return TK_ERR_CUDA;
         }
@@ -1844,3 +1892,99 @@ int tk_net_forward(tk_context* ctx, tk_net* net, const float* x, float* out, flo
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// conv2d_ternary plans (R:linalg.hpp:301-328) on the fused conv kernel: a
+// one-conv plan without ReLU or residual whose f32 NCHW epilogue output is
+// the caller's buffer.  The input packing quantizes with the layer's
+// activation thresholds into the zero-padded channel-last plane (the pad ring
+// is quantize(0.0) = level 0, exactly the reference's zero padding) and
+// reports data errors in the reference's im2col evaluation order; the conv
+// launches as a programmatic dependent of the packing, so its prologue
+// (barriers, TMEM, resident weights) overlaps it.
+
+namespace {
+
+bool single_conv_ok(int C, int OC, int k, int stride, int pad, int h, int w) {
+  if (!(C == 64 || C % 128 == 0) || !(OC == 64 || OC == 128 || OC % 256 == 0)) return false;
+  if (!((k == 3 && pad == 1) || (k == 1 && pad == 0))) return false;
+  if (stride != 1 && stride != 2) return false;
+  if (stride == 2 && ((h % 2) || (w % 2))) return false;
+  if (h < 8 || w < 8) return false;  // a padded plane holds (h+2)(w+2) rows for h*w outputs
+  const int Wp = w + 2;
+  const int span = stride == 1 ? (k == 3 ? 2 * Wp + 2 : 0) : (k == 3 ? Wp / 2 + 1 : 0);
+  return 128 + span <= 256;  // one halo box per 128-position tile
+}
+
+int make_single(const tk_layer* L, int n, int h, int w, tk_net** out) {
+  // int8 weights [out_c][K] in the reference lane order (ky*kw + kx)*in_c + c,
+  // decoded from the packed rows (R:codec.hpp:38-40)
+  std::vector<int8_t> wq((size_t)L->out_c * L->K);
+  for (int o = 0; o < L->out_c; ++o)
+    for (int l = 0; l < L->K; ++l) {
+      const unsigned code = (unsigned)(L->h_words[(size_t)o * L->wpr64 + l / 32] >> (2 * (l % 32))) & 3u;
+      wq[(size_t)o * L->K + l] = (int8_t)(code == 0 ? -1 : (code == 3 ? 1 : 0));
+    }
+  tk_conv_desc d{};
+  d.in_c = L->in_c; d.out_c = L->out_c; d.k = L->kh; d.stride = L->stride; d.pad = L->pad;
+  d.weights_host = wq.data();
+  d.tw1 = L->tw1; d.tw2 = L->tw2; d.ta1 = L->ta1; d.ta2 = L->ta2;
+  d.gain_host = L->h_gain; d.bias_host = L->h_bias;
+  d.out_scale = L->out_scale;
+  tk_net* net = new tk_net;
+  net->ctx = L->ctx;
+  net->batch = n; net->in_c = L->in_c; net->in_h = h; net->in_w = w;
+  net->fused = 1;
+  net->single = 1;
+  const int a = want_s8(net, L->in_c, h, w, d.stride == 2 ? 4 : 1, d.ta1, d.ta2);
+  net->out_c = d.out_c; net->out_h = conv_out(h, d); net->out_w = conv_out(w, d);
+  Conv cv;
+  cv.d = d;
+  cv.in_idx = a;
+  cv.relu = 0;     // conv2d_ternary: folded BN only
+  cv.out_f = -3;   // the caller's output
+  net->convs.assign(1, std::vector<Conv>{cv});
+  int st = finish_fused(net, a, -1);
+  if (st == TK_OK) {
+    PackIn& pk = net->pack;
+    pk.ek = 1; pk.kk = d.k; pk.ks = d.stride; pk.kpad = d.pad; pk.OH = net->out_h; pk.OW = net->out_w;
+    if (cudaDeviceSynchronize() != cudaSuccess) st = TK_ERR_CUDA;
+  }
+  if (st != TK_OK) {
+    tk_net_destroy(net);
+    return st;
+  }
+  *out = net;
+  return TK_OK;
+}
+
+}  // namespace
+
+bool tk_fconv_eligible(const tk_layer* L, int n, int h, int w) {
+  return L && L->nonneg && L->kh == L->kw && n > 0 && encode() != nullptr &&
+         (long long)n * (h + 2) * (w + 2) + 1024 < (1ll << 31) &&
+         single_conv_ok(L->in_c, L->out_c, L->kh, L->stride, L->pad, h, w);
+}
+
+int tk_fconv_run(const tk_layer* L, const float* x, int n, int h, int w, float* out, cudaStream_t s) {
+  tk_net* net = nullptr;
+  {
+    std::lock_guard<std::mutex> lock(L->plan_mu);
+    auto it = L->plans.find({n, h, w});
+    if (it == L->plans.end()) {
+      const int st = make_single(L, n, h, w, &net);
+      if (st != TK_OK) return st;
+      L->plans[{n, h, w}] = net;
+    } else {
+      net = it->second;
+    }
+  }
+  if (launch_pack(net->pack, x, s) != cudaSuccess) return TK_ERR_CUDA;
+  return run_conv(net->convs[0][0], x, out, 1, s) == cudaSuccess ? TK_OK : TK_ERR_CUDA;
+}
+
+void tk_fconv_destroy_plans(tk_layer* L) {
+  std::lock_guard<std::mutex> lock(L->plan_mu);
+  for (auto& kv : L->plans) tk_net_destroy(kv.second);
+  L->plans.clear();
+}

@@ -8,6 +8,8 @@
 // where Z_y counts the zero lanes of the weight row (padding included).
 // M and Z are per weight row, precomputed once at layer creation, so the
 // inner loop is one LOP3 + one POPC + half an IADD3 per u32 word.
+#include <algorithm>
+
 #include "tk_internal.cuh"
 
 namespace {
@@ -17,11 +19,31 @@ __device__ __forceinline__ uint32_t tm_u32(uint32_t x, uint32_t y) {
   return (~(x ^ y) | d) & ~(d << 1);
 }
 
-// cfg1: one warp per vector pair, R:bitkernels.hpp:76-85 (+ :151-159).
-__global__ void k_dot_batched(const uint4* __restrict__ x,
-                              const uint4* __restrict__ y, size_t words,
-                              size_t pairs, const int64_t* __restrict__ wsum,
-                              int64_t* __restrict__ out) {
+// TM with the zero seed supplied (R:bitkernels.hpp:66-72, premask form)
+__device__ __forceinline__ uint32_t tm_seed_u32(uint32_t x, uint32_t y, uint32_t d) {
+  return (~(x ^ y) | d) & ~(d << 1);
+}
+
+template <bool kSeed>
+__device__ __forceinline__ int tm_popc4(const uint4& a, const uint4& b, const uint4& d) {
+  if constexpr (kSeed)
+    return __popc(tm_seed_u32(a.x, b.x, d.x)) + __popc(tm_seed_u32(a.y, b.y, d.y)) +
+           __popc(tm_seed_u32(a.z, b.z, d.z)) + __popc(tm_seed_u32(a.w, b.w, d.w));
+  else
+    return __popc(tm_u32(a.x, b.x)) + __popc(tm_u32(a.y, b.y)) + __popc(tm_u32(a.z, b.z)) +
+           __popc(tm_u32(a.w, b.w));
+}
+
+// cfg1: one warp per vector pair, R:bitkernels.hpp:76-97 (+ :151-159).
+// Streaming-bound (no reuse): a lane issues all loads of a 4 x 16 B chunk of
+// each operand before using any, so a warp keeps (2 or 3) x 2 KB in flight
+// (tools/dot_variants.cu: 5.99 TB/s on cfg1, the read ceiling of this box;
+// the round-1 runtime-trip-count loop kept half that in flight, 4.93 TB/s).
+template <bool kSeed>
+__global__ void __launch_bounds__(256) k_dot_batched(const uint4* __restrict__ x, const uint4* __restrict__ y,
+                                                     const uint4* __restrict__ seed, size_t words, size_t pairs,
+                                                     const int64_t* __restrict__ wsum, int64_t* __restrict__ out) {
+  constexpr int U = 4;  // uint4 per lane per operand in flight
   const int lane = threadIdx.x & 31;
   const size_t warp = (blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5;
   const size_t nwarps = ((size_t)gridDim.x * blockDim.x) >> 5;
@@ -29,27 +51,37 @@ __global__ void k_dot_batched(const uint4* __restrict__ x,
   for (size_t p = warp; p < pairs; p += nwarps) {
     const uint4* xp = x + p * q;
     const uint4* yp = y + p * q;
+    const uint4* dp = kSeed ? seed + p * q : nullptr;
     int acc = 0;
-#pragma unroll 4
-    for (size_t i = lane; i < q; i += 32) {
-      const uint4 a = __ldg(xp + i), b = __ldg(yp + i);
-      acc += __popc(tm_u32(a.x, b.x)) + __popc(tm_u32(a.y, b.y)) +
-             __popc(tm_u32(a.z, b.z)) + __popc(tm_u32(a.w, b.w));
+    for (size_t base = 0; base < q; base += 32 * U) {
+      uint4 a[U], b[U], d[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const size_t i = base + u * 32 + lane;
+        if (i < q) {
+          a[u] = __ldg(xp + i);
+          b[u] = __ldg(yp + i);
+          if constexpr (kSeed) d[u] = __ldg(dp + i);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (base + u * 32 + lane < q) acc += tm_popc4<kSeed>(a[u], b[u], d[u]);
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if (lane == 0) {
-      int64_t r = (int64_t)acc - (int64_t)words * 32;
+      const int64_t r = (int64_t)acc - (int64_t)words * 32;
       out[p] = wsum ? r + wsum[p] : r;
     }
   }
 }
 
 // odd word counts: scalar u64 variant
-__global__ void k_dot_batched_u64(const uint64_t* __restrict__ x,
-                                  const uint64_t* __restrict__ y, size_t words,
-                                  size_t pairs, const int64_t* __restrict__ wsum,
-                                  int64_t* __restrict__ out) {
+template <bool kSeed>
+__global__ void k_dot_batched_u64(const uint64_t* __restrict__ x, const uint64_t* __restrict__ y,
+                                  const uint64_t* __restrict__ seed, size_t words, size_t pairs,
+                                  const int64_t* __restrict__ wsum, int64_t* __restrict__ out) {
   const int lane = threadIdx.x & 31;
   const size_t warp = (blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5;
   const size_t nwarps = ((size_t)gridDim.x * blockDim.x) >> 5;
@@ -57,13 +89,18 @@ __global__ void k_dot_batched_u64(const uint64_t* __restrict__ x,
     int acc = 0;
     for (size_t i = lane; i < words; i += 32) {
       const uint64_t a = x[p * words + i], b = y[p * words + i];
-      acc += __popc(tm_u32((uint32_t)a, (uint32_t)b)) +
-             __popc(tm_u32((uint32_t)(a >> 32), (uint32_t)(b >> 32)));
+      if constexpr (kSeed) {
+        const uint64_t d = seed[p * words + i];
+        acc += __popc(tm_seed_u32((uint32_t)a, (uint32_t)b, (uint32_t)d)) +
+               __popc(tm_seed_u32((uint32_t)(a >> 32), (uint32_t)(b >> 32), (uint32_t)(d >> 32)));
+      } else {
+        acc += __popc(tm_u32((uint32_t)a, (uint32_t)b)) + __popc(tm_u32((uint32_t)(a >> 32), (uint32_t)(b >> 32)));
+      }
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if (lane == 0) {
-      int64_t r = (int64_t)acc - (int64_t)words * 32;
+      const int64_t r = (int64_t)acc - (int64_t)words * 32;
       out[p] = wsum ? r + wsum[p] : r;
     }
   }
@@ -180,23 +217,22 @@ k_gemm_popc(const uint32_t* __restrict__ A, int M, int K32,
 
 }  // namespace
 
-cudaError_t tk_launch_dot_batched(const uint64_t* x, const uint64_t* y,
-                                  size_t words, size_t pairs,
-                                  const int64_t* wsum, int64_t* out,
-                                  cudaStream_t s) {
+cudaError_t tk_launch_dot_batched(const uint64_t* x, const uint64_t* y, const uint64_t* seed, size_t words,
+                                  size_t pairs, const int64_t* wsum, int64_t* out, cudaStream_t s) {
   if (pairs == 0) return cudaSuccess;
-  size_t blocks = (pairs + 7) / 8;  // 8 warps per block
-  if (blocks > 148u * 32u) blocks = 148u * 32u;
-  const bool vec = words % 2 == 0 && ((uintptr_t)x % 16 == 0) &&
-                   ((uintptr_t)y % 16 == 0);
-  if (vec) {
-    k_dot_batched<<<(unsigned)blocks, 256, 0, s>>>(
-        reinterpret_cast<const uint4*>(x), reinterpret_cast<const uint4*>(y),
-        words, pairs, wsum, out);
-  } else {
-    k_dot_batched_u64<<<(unsigned)blocks, 256, 0, s>>>(x, y, words, pairs,
-                                                      wsum, out);
-  }
+  // 8 warps per block, up to 16 resident-block waves of the 148 SMs
+  const size_t blocks = std::min<size_t>((pairs + 7) / 8, 148u * 16u);
+  const bool vec = words % 2 == 0 && ((uintptr_t)x % 16 == 0) && ((uintptr_t)y % 16 == 0) &&
+                   ((uintptr_t)seed % 16 == 0);
+  auto v4 = [](const uint64_t* p) { return reinterpret_cast<const uint4*>(p); };
+  if (vec && seed)
+    k_dot_batched<true><<<(unsigned)blocks, 256, 0, s>>>(v4(x), v4(y), v4(seed), words, pairs, wsum, out);
+  else if (vec)
+    k_dot_batched<false><<<(unsigned)blocks, 256, 0, s>>>(v4(x), v4(y), nullptr, words, pairs, wsum, out);
+  else if (seed)
+    k_dot_batched_u64<true><<<(unsigned)blocks, 256, 0, s>>>(x, y, seed, words, pairs, wsum, out);
+  else
+    k_dot_batched_u64<false><<<(unsigned)blocks, 256, 0, s>>>(x, y, nullptr, words, pairs, wsum, out);
   return cudaGetLastError();
 }
 

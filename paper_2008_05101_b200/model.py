@@ -248,6 +248,11 @@ def packed_forward(m: PackedModel, x, batch: int):
     T.check(T.lib().tk_matmul_t(ctx, xd.data_ptr(), m.stem_w.data_ptr(), m.stem_b.data_ptr(), batch, m.in_dim,
                                 m.hidden, 1, h.data_ptr(), s), "matmul_t (stem)")
     for layer, cal in m.blocks:
+        # a block maps hidden -> hidden: the reference's FC rejects any other
+        # input width (R:linalg.hpp:332-343), and a narrower output would leave
+        # the residual add reading past z (so it is rejected here too)
+        if layer.geom.in_c != m.hidden or layer.geom.out_c != m.hidden:
+            raise tk.InvalidArgument(T.TK_ERR_INVALID, "packed_forward: block width differs from hidden")
         z = tk.fully_connected_ternary(h, batch, layer, check_errors=False)
         T.check(T.lib().tk_residual_relu_rows(ctx, z.data_ptr(), h.data_ptr(), batch * m.hidden, m.hidden,
                                               cal[0].data_ptr() if cal else None,

@@ -45,6 +45,7 @@ class Backend(IntEnum):
     POPC = T.TK_BACKEND_POPC
     TC_I8 = T.TK_BACKEND_TC_I8
     TC_F4 = T.TK_BACKEND_TC_F4
+    TC_CONV = T.TK_BACKEND_TC_CONV  # conv2d_ternary: fused implicit-im2col kernel (kind::i8)
 
 
 @dataclass
@@ -194,18 +195,52 @@ def quant_thresholds(t: QuantThresholds, mode: QuantMode) -> tuple[float, float]
 # inner products
 
 
-def ternary_dot_batched(x: torch.Tensor, y: torch.Tensor, wsum=None) -> torch.Tensor:
+def ternary_dot_batched(x: torch.Tensor, y: torch.Tensor, wsum=None, seeds=None) -> torch.Tensor:
     """x, y: [pairs][words] packed words -> int64 [pairs] (ternary_dot, or
-    ternary_dot_nonneg when wsum is given)."""
+    ternary_dot_nonneg when wsum is given; with `seeds` [pairs][words] the
+    premask form, R:bitkernels.hpp:87-97)."""
     xd, yd = _dev(x, torch.int64), _dev(y, torch.int64)
     if xd.shape != yd.shape:
         raise InvalidArgument(T.TK_ERR_INVALID, "ternary_dot: length mismatch")
     pairs, words = xd.shape
     ws = None if wsum is None else _dev(wsum, torch.int64)
     out = torch.empty(pairs, dtype=torch.int64, device="cuda")
-    check(T.lib().tk_ternary_dot_batched(context(), _p(xd), _p(yd), words, pairs, _p(ws), _p(out),
-                                         _stream()), "ternary_dot")
+    if seeds is None:
+        check(T.lib().tk_ternary_dot_batched(context(), _p(xd), _p(yd), words, pairs, _p(ws), _p(out),
+                                             _stream()), "ternary_dot")
+    else:
+        sd = _dev(seeds, torch.int64).reshape(pairs, words)
+        check(T.lib().tk_ternary_dot_premask_batched(context(), _p(xd), _p(yd), _p(sd), words, pairs, _p(ws),
+                                                     _p(out), _stream()), "ternary_dot_premask")
     return out
+
+
+def ternary_zero_seed(yw: int) -> int:  # R:bitkernels.hpp:47-49
+    return ((yw ^ (yw >> 1)) & kAuxi) & 0xFFFFFFFFFFFFFFFF
+
+
+def ternary_multiply_word(xw: int, yw: int) -> int:  # R:bitkernels.hpp:55-63
+    return ternary_multiply_word_premask(xw, yw, ternary_zero_seed(yw))
+
+
+def ternary_multiply_word_premask(xw: int, yw: int, d: int) -> int:  # R:bitkernels.hpp:66-72
+    m = 0xFFFFFFFFFFFFFFFF
+    return ((~(xw ^ yw) & m) | d) & ~(d << 1) & m
+
+
+def ternary_dot_words(x, y, words: int | None = None) -> int:
+    """detail::ternary_dot_words (R:bitkernels.hpp:76-85): raw word buffers."""
+    xd, yd = _dev(x, torch.int64).reshape(-1), _dev(y, torch.int64).reshape(-1)
+    n = xd.numel() if words is None else words
+    return int(ternary_dot_batched(xd[:n].view(1, -1), yd[:n].view(1, -1)).item())
+
+
+def ternary_dot_words_premask(x, y, seed, words: int | None = None) -> int:
+    """detail::ternary_dot_words_premask (R:bitkernels.hpp:87-97)."""
+    xd, yd = _dev(x, torch.int64).reshape(-1), _dev(y, torch.int64).reshape(-1)
+    sd = _dev(seed, torch.int64).reshape(-1)
+    n = xd.numel() if words is None else words
+    return int(ternary_dot_batched(xd[:n].view(1, -1), yd[:n].view(1, -1), seeds=sd[:n].view(1, -1)).item())
 
 
 def ternary_dot(x: PackedTernaryVector, y: PackedTernaryVector) -> int:
@@ -216,18 +251,19 @@ def ternary_dot(x: PackedTernaryVector, y: PackedTernaryVector) -> int:
 
 
 def make_zero_seeds(y: PackedTernaryVector) -> torch.Tensor:
-    """R:bitkernels.hpp:127-134 (device words; used only for the length check)."""
+    """R:bitkernels.hpp:127-134 (device words)."""
     w = y.words
     return (w ^ (w >> 1)) & kAuxi
 
 
 def ternary_dot_premask(x: PackedTernaryVector, y: PackedTernaryVector, seeds) -> int:
-    """R:bitkernels.hpp:136-147: identical integers to ternary_dot."""
+    """R:bitkernels.hpp:136-147: the TM uses the supplied seeds as given."""
     if x.logical_len != y.logical_len:
         raise InvalidArgument(T.TK_ERR_INVALID, "ternary_dot_premask: length mismatch")
     if len(seeds) != y.words.numel():
         raise InvalidArgument(T.TK_ERR_INVALID, "ternary_dot_premask: seed buffer mismatch")
-    return ternary_dot(x, y)
+    return int(ternary_dot_batched(x.words.view(1, -1), y.words.view(1, -1),
+                                   seeds=_dev(seeds, torch.int64).view(1, -1)).item())
 
 
 def ternary_dot_nonneg(a: PackedTernaryVector, w: PackedTernaryVector, w_sum: int) -> int:

@@ -129,6 +129,28 @@ static void bitkernels() {
   PackedTernaryVector ap = pack(st);
   ap.nonneg_offset = true;
   CHECK(ternary_dot_nonneg(ap, pack(std::vector<std::int8_t>{1, -1, 1}), 1) == 3);
+  // R:bitkernels.hpp:66-97: the raw-pointer detail:: entries and the premask
+  // forms; with make_zero_seeds they equal ternary_dot, and supplied seeds are
+  // used as given (here: all-zero seeds = every lane treated as nonzero)
+  {
+    const std::vector<std::int8_t> xs = random_ternary(1000, 21), ys = random_ternary(1000, 22);
+    const PackedTernaryVector xp = pack(xs), yp = pack(ys);
+    const std::vector<std::uint64_t> seeds = make_zero_seeds(yp);
+    const std::int64_t want = ternary_dot(xp, yp);
+    CHECK(detail::ternary_dot_words(xp.words.data(), yp.words.data(), xp.words.size()) == want);
+    CHECK(detail::ternary_dot_words_premask(xp.words.data(), yp.words.data(), seeds.data(), xp.words.size()) == want);
+    CHECK(ternary_dot_premask(xp, yp, seeds) == want);
+    const std::vector<std::uint64_t> zero(seeds.size(), 0);
+    std::int64_t host = 0;
+    for (std::size_t i = 0; i < xp.words.size(); ++i)
+      host += __builtin_popcountll(ternary_multiply_word_premask(xp.words[i], yp.words[i], 0));
+    host -= static_cast<std::int64_t>(xp.words.size()) * kLanesPerWord;
+    CHECK(ternary_dot_premask(xp, yp, zero) == host);
+    CHECK(detail::ternary_dot_words_premask(xp.words.data(), yp.words.data(), zero.data(), xp.words.size()) == host);
+    for (std::size_t i = 0; i < xp.words.size(); ++i)
+      CHECK(ternary_multiply_word_premask(xp.words[i], yp.words[i], seeds[i]) ==
+            ternary_multiply_word(xp.words[i], yp.words[i]));
+  }
 }
 
 static void linalg() {

@@ -138,3 +138,29 @@ def test_batched_dot_cfg1_vs_oracle(tk, oracle):
     assert np.array_equal(got, want)
     al = np.stack([oracle.unpack(r, n) for r in u64(aw)[:64]]).astype(np.int64) + 1
     assert np.array_equal(got[:64], (al * wl).sum(1))
+
+
+@pytest.mark.parametrize("words", [1, 2, 3, 7, 64, 128, 129, 300, 1000])
+def test_batched_dot_ragged_words_and_premask(tk, oracle, words):
+    """Word counts around the kernel's 4 x 16 B per-lane chunks (odd counts
+    take the u64 kernel), the cfg1 row (128) and rows longer than one chunk;
+    the premask form (R:bitkernels.hpp:66-72, :87-97) with make_zero_seeds
+    equals ternary_dot and with arbitrary seeds equals the host TM formula."""
+    rng = np.random.default_rng(words)
+    pairs = 257
+    x = rng.integers(0, 2**63, (pairs, words), dtype=np.uint64) * np.uint64(2) + rng.integers(0, 2, (pairs, words),
+                                                                                               dtype=np.uint64)
+    y = rng.integers(0, 2**63, (pairs, words), dtype=np.uint64) * np.uint64(2) + rng.integers(0, 2, (pairs, words),
+                                                                                               dtype=np.uint64)
+    ws = rng.integers(-5000, 5000, pairs).astype(np.int64)
+    got = tk.ternary_dot_batched(x, y, ws).cpu().numpy()
+    assert np.array_equal(got, oracle.ternary_dot_batched(x, y, ws))
+    seeds = (y ^ (y >> np.uint64(1))) & np.uint64(tk.kAuxi)
+    assert np.array_equal(tk.ternary_dot_batched(x, y, ws, seeds=seeds).cpu().numpy(), got)
+    rs = rng.integers(0, 2**63, (pairs, words), dtype=np.uint64) & np.uint64(tk.kAuxi)  # arbitrary seeds
+    tm = (~(x ^ y) | rs) & ~(rs << np.uint64(1))
+    want = np.bitwise_count(tm).sum(axis=1, dtype=np.int64) - 32 * words + ws
+    assert np.array_equal(tk.ternary_dot_batched(x, y, ws, seeds=rs).cpu().numpy(), want)
+    # detail:: raw-word entries on one pair
+    assert tk.ternary_dot_words(x[0], y[0]) == int(got[0] - ws[0])
+    assert tk.ternary_dot_words_premask(x[0], y[0], rs[0]) == int(want[0] - ws[0])

@@ -45,7 +45,7 @@ def test_im2col_kats(tk, golden):
                                 QM.kWeight)
 
 
-@pytest.mark.parametrize("backend", ["POPC", "TC_I8", "TC_F4"])
+@pytest.mark.parametrize("backend", ["POPC", "TC_I8", "TC_F4", "TC_CONV"])
 def test_conv_shapes_golden(tk, golden, backend):
     QT, QM, TS, CG = tk.QuantThresholds, tk.QuantMode, tk.TensorShape, tk.ConvGeometry
     for i, (c, r, k, s, p, b) in enumerate(golden["conv_shapes"]):
@@ -111,7 +111,7 @@ def test_selector_row(tk):
     assert list(out) == want
 
 
-@pytest.mark.parametrize("backend", ["POPC", "TC_I8", "TC_F4"])
+@pytest.mark.parametrize("backend", ["POPC", "TC_I8", "TC_F4", "TC_CONV"])
 def test_conv_properties(tk, oracle, backend):
     """Batch independence (exact), out_scale linearity, geometry grid, zero-input FC
     (R:tests/test_linalg.cpp:267-380)."""
@@ -265,3 +265,71 @@ def test_fp4_operand_errors_and_stream_order(tk):
         torch.cuda.synchronize()
         outs[be.name] = y.cpu().numpy()
     assert np.array_equal(outs["TC_F4"].view(np.int32), outs["POPC"].view(np.int32))
+
+
+FUSED_CASES = [  # (c, oc, h, w, k, stride, n)
+    (64, 64, 56, 56, 3, 1, 1),     # cfg2
+    (64, 64, 56, 56, 3, 1, 3),
+    (64, 128, 28, 28, 3, 2, 2),
+    (128, 128, 14, 14, 3, 1, 2),
+    (128, 256, 14, 14, 1, 2, 2),
+    (256, 512, 8, 8, 3, 1, 1),
+    (64, 64, 9, 10, 3, 1, 2),
+    (128, 64, 12, 8, 1, 1, 3),
+]
+
+
+@pytest.mark.parametrize("c,oc,h,w,k,s,n", FUSED_CASES)
+def test_conv2d_fused_implicit_im2col(tk, oracle, c, oc, h, w, k, s, n):
+    """conv2d_ternary on the fused implicit-im2col kernel (AUTO / TC_CONV):
+    f32 NCHW output bit-identical to the oracle (R:linalg.hpp:301-328) and to
+    the explicit-im2col GEMM pipes, incl. stride 2, 1x1, two N tiles, ragged
+    planes and a batch whose last M tile is partial."""
+    rng = np.random.default_rng(c + oc + h + w + k + s + n)
+    wq = rng.integers(-1, 2, (oc, c * k * k)).astype(np.int8)
+    gain = (rng.uniform(0.5, 1.5, oc) / 16).astype(np.float32)
+    bias = rng.standard_normal(oc).astype(np.float32)
+    x = np.abs(rng.standard_normal(n * c * h * w)).astype(np.float32)
+    x[:: 97] = 0.0
+    shape = tk.TensorShape(n, c, h, w)
+    st, want = oracle.conv2d_ternary(x, n, c, h, w, wq, oc, k, s, k // 2, (0.5, 0.9), True, gain, bias, 0.37)
+    assert st == 0
+    for be in ("AUTO", "TC_CONV", "TC_I8"):
+        layer = _layer(tk, wq, c, oc, k, s, k // 2, gain=gain, bias=bias, out_scale=0.37)
+        layer.set_backend(tk.Backend[be])
+        y = tk.conv2d_ternary(x, shape, layer).data.cpu().numpy()
+        y2 = tk.conv2d_ternary(x, shape, layer).data.cpu().numpy()  # the cached plan again
+        assert np.array_equal(y.view(np.int32), want.view(np.int32)), be
+        assert np.array_equal(y2.view(np.int32), y.view(np.int32)), be
+
+
+def test_conv2d_fused_errors_in_reference_order(tk, oracle):
+    """Data errors on the fused path report the reference's FIRST error in its
+    im2col evaluation order (R:linalg.hpp:173-225, R:quantizer.hpp:37-41,53-55),
+    not the first in memory order: a negative value used by output row 0
+    wins over a NaN at a smaller NCHW index first used by a later row (and
+    the reverse); a bad value no patch reads (1x1 / stride 2 skips odd rows
+    and columns) raises nothing."""
+    from paper_2008_05101_b200 import _lib as T
+    c, h, w = 64, 16, 16
+    wq = np.random.default_rng(1).integers(-1, 2, (64, c * 9)).astype(np.int8)
+    layer = _layer(tk, wq, c, 64, 3, 1, 1)
+    layer.set_backend(tk.Backend.TC_CONV)
+    for neg, nan, code in [((63, 0, 0), (0, 5, 5), T.TK_ERR_NEGATIVE), ((0, 9, 9), (63, 0, 1), T.TK_ERR_NONFINITE)]:
+        x = np.abs(np.random.default_rng(2).standard_normal((1, c, h, w))).astype(np.float32)
+        x[(0, *neg)] = -1.0
+        x[(0, *nan)] = np.nan
+        st, _ = oracle.conv2d_ternary(x.reshape(-1), 1, c, h, w, wq, 64, 3, 1, 1, (0.5, 0.9), True)
+        assert st == code
+        with pytest.raises(tk.InvalidArgument) as ei:
+            tk.conv2d_ternary(x.reshape(-1), tk.TensorShape(1, c, h, w), layer)
+        assert ei.value.status == code
+    w1 = np.random.default_rng(4).integers(-1, 2, (128, c)).astype(np.int8)
+    l1 = _layer(tk, w1, c, 128, 1, 2, 0)
+    l1.set_backend(tk.Backend.TC_CONV)
+    x3 = np.abs(np.random.default_rng(5).standard_normal((2, c, h, w))).astype(np.float32)
+    x3[1, 7, 3, 5] = -1.0
+    st3, want = oracle.conv2d_ternary(x3.reshape(-1), 2, c, h, w, w1, 128, 1, 2, 0, (0.5, 0.9), True)
+    assert st3 == 0
+    y = tk.conv2d_ternary(x3.reshape(-1), tk.TensorShape(2, c, h, w), l1).data.cpu().numpy()
+    assert np.array_equal(y.view(np.int32), want.view(np.int32))

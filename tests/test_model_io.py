@@ -76,3 +76,23 @@ def test_packed_forward_gpu_matches_reference(tk, golden, tag):
     want = golden["pf_logits" if tag == "cal" else "pf_logits_nocal"]
     assert np.array_equal(logits.view(np.int32), want.view(np.int32))
     assert np.array_equal(argmax_rows(logits), want.argmax(axis=1))
+
+
+@pytest.mark.gpu
+def test_packed_forward_rejects_block_width_mismatch(tk, golden):
+    """A block whose width differs from `hidden` is an InvalidArgument (the
+    reference's FC size check, R:linalg.hpp:332-343), never an out-of-bounds
+    residual add."""
+    import dataclasses
+    from paper_2008_05101_b200.model import PackedModel, packed_forward
+    spec = parse_model(fixture("nocal"))
+    b0 = spec.blocks[0]
+    out_c = b0.out_c - 1
+    wpr = b0.words.shape[1]
+    narrow = dataclasses.replace(b0, out_c=out_c, words=b0.words[:out_c].copy(), weight_sums=b0.weight_sums[:out_c],
+                                 gain=b0.gain[:out_c], bias=b0.bias[:out_c])
+    assert narrow.words.shape == (out_c, wpr)
+    m = PackedModel(dataclasses.replace(spec, blocks=[narrow] + spec.blocks[1:]))
+    batch = int(golden["pf_dims"][0])
+    with pytest.raises(tk.InvalidArgument):
+        packed_forward(m, golden["pf_x"], batch)
