@@ -522,234 +522,6 @@ k_gemm_tc_i8(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
   }
 }
 
-// ---------------------------------------------------------------------------
-// Weights-stationary GEMM for few activation rows (FC batches, M <= 256):
-// the MMA's M side is 128 WEIGHT rows (output channels) and its N side the
-// whole batch (NB = 64 / 128 / 256 rows of the activation operand), so each
-// CTA reads its 128 weight rows once and the batch once per K range -- the
-// activation-stationary kernel above re-reads the batch operand once per
-// 64-wide weight tile (cfg3: 49 MB of L2 -> SM traffic for 8.4 MB of
-// operands; here 24.6 MB).  The K range is split S ways over the CTAs of a
-// (1, 1, S) cluster; s16 partials (|partial| <= 2 * levels per CTA < 2^15,
-// checked at launch) go to the CTA owning their batch columns over DSMEM,
-// and each CTA sums its S slices, applies the epilogue per output channel
-// (a thread per channel: consecutive lanes write consecutive outputs of one
-// batch row) and stores y[batch][channel].
-template <int NB, bool F4>
-struct WtSmem {
-  static constexpr int kA = BM * 128;  // one K block of 128 weight rows (128 B per row)
-  static constexpr int kB = NB * 128;  // one K block of the batch
-  static constexpr int kStage = kA + kB;
-  static constexpr int kStages = (196 * 1024 / kStage) > 8 ? 8 : (196 * 1024 / kStage);
-  static constexpr int kRecv = BM * NB * 2;  // s16 [S][128][NB/S]
-  static constexpr int kRing = kStages * kStage > kRecv ? kStages * kStage : kRecv;
-  static constexpr int kBytes = kRing + 1024 /*align*/ + 256 /*barriers*/;
-  // accumulator columns (+ unit scale-factor columns for kind::mxf4)
-  static constexpr uint32_t kCols = F4 ? (NB <= 128 ? 256 : 512) : (NB < 32 ? 32 : NB);
-};
-
-template <int NB, bool F4>
-__global__ void __launch_bounds__(kThreads, 1)
-k_gemm_wt(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX, int M, int N,
-          int num_kb, int m_pad, int n_pad, int S, tk_epilogue e) {
-  using SM = WtSmem<NB, F4>;
-  constexpr int kStages = SM::kStages;
-  constexpr uint32_t kCols = SM::kCols;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = smem_raw + ((1024u - (sm100::smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + SM::kRing);
-  uint64_t* empty = full + kStages;
-  uint64_t* tmem_full = empty + kStages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int o0 = blockIdx.x * BM;  // first output channel of this CTA
-  const int z = blockIdx.z;        // K split == rank in the (1, 1, S) cluster
-  const int kb0 = (int)((long long)z * num_kb / S), kb1 = (int)((long long)(z + 1) * num_kb / S);
-  const int nkb = kb1 - kb0;
-
-  if (threadIdx.x == 0) {
-    sm100::tma_prefetch(&tmW);
-    sm100::tma_prefetch(&tmX);
-    for (int s = 0; s < kStages; ++s) {
-      sm100::mbar_init(&full[s], 1);
-      sm100::mbar_init(&empty[s], 1);
-    }
-    sm100::mbar_init(tmem_full, 1);
-    sm100::fence_mbar_init();
-  }
-  __syncthreads();
-  uint32_t tmem = 0;
-  if (warp >= 1) {  // TMEM (+ unit scales) while the producer starts loading
-    if (warp == 1) sm100::tmem_alloc<kCols>(tmem_slot);
-    sm100::tc_fence_before();
-    sm100::named_bar_sync(1, kThreads - 32);
-    sm100::tc_fence_after();
-    tmem = *tmem_slot;
-    if constexpr (F4) {
-      if (warp >= 2 && warp < 6)
-        sm100::tmem_fill_unit_scales<kCols - NB>(tmem + ((uint32_t)((warp & 3) * 32) << 16) + NB);
-      sm100::tc_fence_before();
-      sm100::named_bar_sync(1, kThreads - 32);
-      sm100::tc_fence_after();
-    }
-  }
-  if (warp == 0) {
-    // ---- TMA producer: the weight boxes of the first stages go out before
-    // griddepcontrol.wait (they do not depend on the previous kernel)
-    const int npre = min(kStages, nkb);
-    if (lane == 0)
-      for (int i = 0; i < npre; ++i) {
-        sm100::mbar_arrive_expect_tx(&full[i], SM::kStage);
-        sm100::tma_load_2d(smem + i * SM::kStage, &tmW, &full[i], 0, (kb0 + i) * n_pad + o0);
-      }
-    sm100::pdl_wait();
-    int s = 0, round = 0;
-    for (int i = 0; i < nkb; ++i) {
-      if (round) sm100::mbar_wait(&empty[s], (round - 1) & 1);
-      if (lane == 0) {
-        uint8_t* st = smem + s * SM::kStage;
-        if (i >= npre) {
-          sm100::mbar_arrive_expect_tx(&full[s], SM::kStage);
-          sm100::tma_load_2d(st, &tmW, &full[s], 0, (kb0 + i) * n_pad + o0);
-        }
-        sm100::tma_load_2d(st + SM::kA, &tmX, &full[s], 0, (kb0 + i) * m_pad);
-      }
-      __syncwarp();
-      if (++s == kStages) { s = 0; ++round; }
-    }
-  } else if (warp == 1) {
-    // ---- MMA issuer: 4 x (128 x NB x 32 bytes of K) per K block
-    constexpr uint32_t idesc = F4 ? sm100::idesc_f4(BM, NB) : sm100::idesc_i8(BM, NB);
-    int s = 0, round = 0;
-    for (int i = 0; i < nkb; ++i) {
-      sm100::mbar_wait(&full[s], round & 1);
-      sm100::tc_fence_after();
-      const uint32_t a0 = sm100::smem_u32(smem + s * SM::kStage), b0 = a0 + SM::kA;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        if constexpr (F4)
-          sm100::mma_f4_elect(tmem, sm100::desc_k_sw128(a0 + k * 32), sm100::desc_k_sw128(b0 + k * 32), idesc,
-                              (i > 0 || k > 0) ? 1u : 0u, tmem + NB, tmem + NB + 64);
-        else
-          sm100::mma_i8_elect(tmem, sm100::desc_k_sw128(a0 + k * 32), sm100::desc_k_sw128(b0 + k * 32), idesc,
-                              (i > 0 || k > 0) ? 1u : 0u);
-      }
-      sm100::mma_commit_elect(&empty[s]);
-      if (++s == kStages) { s = 0; ++round; }
-    }
-    sm100::mma_commit_elect(tmem_full);
-  }
-  const bool f32 = e.mode != TK_EPI_I32;
-  if (S == 1) {
-    // ---- one K range: TMEM row (channel) -> epilogue -> y[b][o], lanes = channels
-    if (warp >= 2) {
-      const int q = warp & 3, half = (warp - 2) >> 2;
-      const int o = o0 + q * 32 + lane;
-      const float g = f32 && o < N ? __ldg(e.gain + o) : 0.0f, b = f32 && o < N ? __ldg(e.bias + o) : 0.0f;
-      sm100::pdl_wait();
-      sm100::mbar_wait(tmem_full, 0);
-      sm100::tc_fence_after();
-      constexpr int kHalf = NB / 2 < 32 ? 32 : NB / 2;
-#pragma unroll 1
-      for (int c0 = half * kHalf; c0 < (half + 1) * kHalf && c0 < NB; c0 += 32) {
-        uint32_t r[32];
-        sm100::tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + c0, r);
-        sm100::tmem_ld_wait();
-        if (o >= N) continue;
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          if (c0 + j >= M) break;
-          const int acc = F4 ? __float2int_rn(__uint_as_float(r[j])) : (int)r[j];
-          if (f32)  // R:linalg.hpp:322-323 with the reference build's FMA contraction
-            static_cast<float*>(e.out)[(size_t)(c0 + j) * N + o] = __fmaf_rn(g, __fmul_rn(e.out_scale, (float)acc), b);
-          else
-            static_cast<int32_t*>(e.out)[(size_t)(c0 + j) * N + o] = acc;
-        }
-      }
-    }
-    sm100::tc_fence_before();
-    __syncthreads();
-    if (warp == 1) sm100::tmem_dealloc<kCols>(tmem);
-    return;
-  }
-  // ---- split-K exchange: batch columns [r * cs, (r + 1) * cs) belong to
-  // cluster rank r.  Receive layout [src][row][cs / 8 chunks of 16 B], chunks
-  // XOR-swizzled by row so a warp's 32 row-stores spread over the banks.
-  const int cs = NB / S, C8 = cs / 8;
-  auto swz = [C8](int row, int c) { return C8 >= 8 ? ((c & ~7) | ((c ^ row) & 7)) : c; };
-  uint4* recv = reinterpret_cast<uint4*>(smem);
-  if (warp >= 1) sm100::pdl_wait();
-  if (warp >= 2) sm100::mbar_wait(tmem_full, 0);
-  sm100::tc_fence_before();
-  sm100::cluster_sync();  // every CTA's MMAs are done: all operand rings are free
-  if (warp >= 2) {
-    sm100::tc_fence_after();
-    const int q = warp & 3, half = (warp - 2) >> 2;
-    const int row = q * 32 + lane;
-    constexpr int kHalf = NB / 2 < 32 ? 32 : NB / 2;
-#pragma unroll 1
-    for (int c0 = half * kHalf; c0 < (half + 1) * kHalf && c0 < NB; c0 += 32) {
-      uint32_t r[32];
-      sm100::tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + c0, r);
-      sm100::tmem_ld_wait();
-      if constexpr (F4) {  // f32 accumulators of exact integers (|v| < 2^15)
-#pragma unroll
-        for (int j = 0; j < 32; ++j) r[j] = (uint32_t)__float2int_rn(__uint_as_float(r[j]));
-      }
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int c = c0 + 8 * j, owner = c / cs, cc = (c - owner * cs) / 8;
-        uint32_t w[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) w[i] = (r[8 * j + 2 * i] & 0xFFFFu) | (r[8 * j + 2 * i + 1] << 16);
-        const uint32_t a = sm100::smem_u32(recv + (size_t)(z * BM + row) * C8 + swz(row, cc));
-        if (owner == z)
-          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(w[0]), "r"(w[1]), "r"(w[2]),
-                       "r"(w[3])
-                       : "memory");
-        else
-          sm100::st_cluster_v4(a, (uint32_t)owner, make_uint4(w[0], w[1], w[2], w[3]));
-      }
-    }
-  }
-  sm100::cluster_sync();
-  // ---- reduce + epilogue over the owned columns: thread = channel row (fixed
-  // across iterations), chunks of 8 batch columns
-  if (warp >= 2) {
-    const int et = threadIdx.x - 64;
-    const int row = et & (BM - 1), o = o0 + row;
-    const float g = f32 && o < N ? __ldg(e.gain + o) : 0.0f, b = f32 && o < N ? __ldg(e.bias + o) : 0.0f;
-    if (o < N) {
-#pragma unroll 1
-      for (int cc = et >> 7; cc < C8; cc += (kThreads - 64) / BM) {
-        int acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-#pragma unroll 1
-        for (int src = 0; src < S; ++src) {
-          const uint4 v = recv[(size_t)(src * BM + row) * C8 + swz(row, cc)];
-          const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            acc[2 * i] += (int)(int16_t)(w[i] & 0xFFFFu);
-            acc[2 * i + 1] += (int)w[i] >> 16;
-          }
-        }
-        const int bb = z * cs + cc * 8;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          if (bb + j >= M) break;
-          if (f32)  // R:linalg.hpp:322-323 with the reference build's FMA contraction
-            static_cast<float*>(e.out)[(size_t)(bb + j) * N + o] = __fmaf_rn(g, __fmul_rn(e.out_scale, (float)acc[j]), b);
-          else
-            static_cast<int32_t*>(e.out)[(size_t)(bb + j) * N + o] = acc[j];
-        }
-      }
-    }
-  }
-  sm100::tc_fence_before();
-  __syncthreads();
-  if (warp == 1) sm100::tmem_dealloc<kCols>(tmem);
-}
-
 // ---- host side: tensor maps through the driver entry point ----------------
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                               const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -867,32 +639,6 @@ cudaError_t launch(const int8_t* a, int M, int num_kb, const tk_layer* L, tk_epi
                             dbg);
 }
 
-// weights-stationary launch (k_gemm_wt): row-major outputs of <= 256 rows
-template <int NB, bool F4>
-cudaError_t launch_wt(const int8_t* a, int M, int num_kb, const tk_layer* L, tk_epilogue e, int S, cudaStream_t s) {
-  CUtensorMap tw, tx;
-  const int m_pad = (M + BM - 1) / BM * BM;
-  if (!make_map(&tw, F4 ? L->d_w4 : L->d_w8, (uint64_t)num_kb * L->n_pad, 128, BM)) return cudaErrorInvalidValue;
-  if (!make_map(&tx, a, (uint64_t)num_kb * m_pad, 128, NB)) return cudaErrorInvalidValue;
-  using SM = WtSmem<NB, F4>;
-  if (const cudaError_t er = tk_smem_attr((const void*)k_gemm_wt<NB, F4>, SM::kBytes); er != cudaSuccess) return er;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((L->out_c + BM - 1) / BM, 1, S);
-  cfg.blockDim = dim3(kThreads, 1, 1);
-  cfg.dynamicSmemBytes = SM::kBytes;
-  cfg.stream = s;
-  cudaLaunchAttribute at[2];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = 1;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = S;
-  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[1].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 2;
-  return cudaLaunchKernelEx(&cfg, k_gemm_wt<NB, F4>, tw, tx, M, L->out_c, num_kb, m_pad, L->n_pad, S, e);
-}
-
 }  // namespace
 
 // K blocks one CTA may accumulate: its s16 partial |sum| <= 2*128*blocks < 2^15
@@ -915,25 +661,6 @@ cudaError_t tk_launch_gemm_tc_fmt(const int8_t* a_s8, int M, int k_pad, const tk
   const long tiles_m = (M + BM - 1) / BM;
   const int N = L->out_c, num_kb = fp4 ? k_pad / 256 : k_pad / BK;
   const int max_kb = fp4 ? kMaxKbPerCta / 2 : kMaxKbPerCta;  // 256 levels per fp4 K block
-  // Few rows, many output channels (FC batches): weights-stationary tiles,
-  // the batch as the MMA's N side, K split across a cluster until >= 96 CTAs
-  // (or the s16 partial bound) -- DESIGN.md 4.4
-  const int wt_tiles = (N + BM - 1) / BM;
-  if (e.mode != TK_EPI_F32_NCHW && M <= 256 && wt_tiles >= 12 && !tk_knob("TK_GEMM_NOWT", 0)) {
-    int S = 1;
-    while (S < 8 && (wt_tiles * S < 96 || (num_kb + S - 1) / S > max_kb) && 2 * S <= num_kb) S *= 2;
-    if ((num_kb + S - 1) / S <= max_kb || S == 1) {
-      const int NB = M <= 64 ? 64 : (M <= 128 ? 128 : 256);
-      if (S == 1 || NB / S >= 8) {
-        if (fp4) return NB == 64 ? launch_wt<64, true>(a_s8, M, num_kb, L, e, S, s)
-                     : NB == 128 ? launch_wt<128, true>(a_s8, M, num_kb, L, e, S, s)
-                                 : launch_wt<256, true>(a_s8, M, num_kb, L, e, S, s);
-        return NB == 64 ? launch_wt<64, false>(a_s8, M, num_kb, L, e, S, s)
-             : NB == 128 ? launch_wt<128, false>(a_s8, M, num_kb, L, e, S, s)
-                         : launch_wt<256, false>(a_s8, M, num_kb, L, e, S, s);
-      }
-    }
-  }
   const bool no_direct = tk_knob("TK_GEMM_NODIRECT", 0) != 0;
   const bool row_major = !no_direct && e.mode != TK_EPI_F32_NCHW && N % 4 == 0 && (uintptr_t)e.out % 16 == 0;
   auto tiles_of = [&](int bn) { return tiles_m * ((N + bn - 1) / bn); };

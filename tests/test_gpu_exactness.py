@@ -135,11 +135,11 @@ def test_layer_build_matches_reference(tk, c, oc, k):
 @pytest.mark.parametrize("fmt", ["s8", "fp4"])
 @pytest.mark.parametrize("rows,k", [(256, 4096), (256, 40000), (200, 16384), (128, 4096), (100, 40000), (64, 8192),
                                     (37, 4096), (1, 40000)])
-def test_worst_case_weights_stationary(tk, rows, k, fmt):
-    """The weights-stationary FC kernel (<= 256 rows, >= 12 tiles of 128
-    output channels: the cfg3 path) across its batch tiles (64 / 128 / 256)
-    and K splits (up to 8-CTA clusters), at worst-case magnitudes, with the
-    int32 and the fused f32 epilogue (gain 1, bias 0: y == acc)."""
+def test_worst_case_fc_shapes(tk, rows, k, fmt):
+    """FC-shaped GEMMs (<= 256 rows, 2048-4096 output channels: the cfg3
+    family) across the launcher's tile / split-K choices at worst-case
+    magnitudes, with the int32 and the fused f32 epilogue (gain 1, bias 0:
+    y == acc)."""
     cols = 2048 if k > 4096 else 4096
     L, W, want = worst_case(k, rows=rows, cols=cols, seed=3)
     layer = _layer(tk, W, k, gain=np.ones(cols, np.float32))
