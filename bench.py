@@ -411,10 +411,10 @@ class DotWorkload:
         self.config = {"workload": f"cfg1 ternary inner product N={n}, {pairs} packed pairs "
                                    "(ternary_dot_nonneg, LOP3+POPC)", "n": n, "pairs": pairs,
                        "alpha_x": [0.5, 0.9], "alpha_y": [0.8, 1.2],
-                       "l2": "flushed between steps (256 MB write; the packed operands, 134 MB, exceed the "
-                             "126 MB L2 anyway -- the flush also keeps the GPU busy while the host enqueues "
-                             "the step, so the events time the kernel, not the launch)"}
-        self.needs_flush = True
+                       "l2": "not flushed: the step's packed operands (134 MB) exceed the 126 MB L2 (a 256 MB "
+                             "write flush would leave ~126 MB of dirty lines whose write-back then competes "
+                             "with the step's reads)"}
+        self.needs_flush = False
 
     @staticmethod
     def _wsum_host(words_u64, n):
@@ -650,9 +650,9 @@ class ResNetWorkload:
                        "body_gmac_per_img": round(self.macs_per_img / 1e9, 4),
                        "e2e_slices": {"chunks": chunks, "body_groups": groups}}
         in_mb = batch * 64 * 56 * 56 * 4 / 2**20
-        self.needs_flush = True
-        self.config["l2"] = (f"flushed between steps (256 MB write; the step's input is {in_mb:.0f} MB f32) -- "
-                             "the flush also keeps the GPU busy while the host launches the step's graph")
+        self.needs_flush = in_mb <= 126
+        self.config["l2"] = ("flushed between steps (256 MB write)" if self.needs_flush else
+                             f"not flushed: the step's input ({in_mb:.0f} MB f32) exceeds the 126 MB L2")
 
     def step(self):
         return self.net.body.forward(self.x, pooled=self.pooled, check_errors=False)
