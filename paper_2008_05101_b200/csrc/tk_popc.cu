@@ -77,6 +77,38 @@ __global__ void __launch_bounds__(256) k_dot_batched(const uint4* __restrict__ x
   }
 }
 
+// Rows of exactly 32 * L uint4 (N = 2048 / 4096 / 8192 lanes: the cfg1 row
+// is L = 2): the trip count is a compile-time constant, so every load of a
+// lane is issued before any use with no predication (tools/dot_variants.cu
+// "v1 P1": 5.99 TB/s on cfg1 vs 4.93 for a runtime-bounded loop).
+template <int L, bool kSeed>
+__global__ void __launch_bounds__(256) k_dot_fixed(const uint4* __restrict__ x, const uint4* __restrict__ y,
+                                                   const uint4* __restrict__ seed, size_t pairs,
+                                                   const int64_t* __restrict__ wsum, int64_t* __restrict__ out) {
+  constexpr int Q = 32 * L;
+  const int lane = threadIdx.x & 31;
+  const size_t warp = (blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5;
+  const size_t nwarps = ((size_t)gridDim.x * blockDim.x) >> 5;
+  for (size_t p = warp; p < pairs; p += nwarps) {
+    uint4 a[L], b[L], d[L];
+#pragma unroll
+    for (int i = 0; i < L; ++i) {
+      a[i] = __ldg(x + p * Q + i * 32 + lane);
+      b[i] = __ldg(y + p * Q + i * 32 + lane);
+      if constexpr (kSeed) d[i] = __ldg(seed + p * Q + i * 32 + lane);
+    }
+    int acc = 0;
+#pragma unroll
+    for (int i = 0; i < L; ++i) acc += tm_popc4<kSeed>(a[i], b[i], d[i]);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) {
+      const int64_t r = (int64_t)acc - (int64_t)Q * 2 * 32;
+      out[p] = wsum ? r + wsum[p] : r;
+    }
+  }
+}
+
 // odd word counts: scalar u64 variant
 template <bool kSeed>
 __global__ void k_dot_batched_u64(const uint64_t* __restrict__ x, const uint64_t* __restrict__ y,
@@ -225,7 +257,20 @@ cudaError_t tk_launch_dot_batched(const uint64_t* x, const uint64_t* y, const ui
   const bool vec = words % 2 == 0 && ((uintptr_t)x % 16 == 0) && ((uintptr_t)y % 16 == 0) &&
                    ((uintptr_t)seed % 16 == 0);
   auto v4 = [](const uint64_t* p) { return reinterpret_cast<const uint4*>(p); };
-  if (vec && seed)
+  if (vec && (words == 64 || words == 128 || words == 256)) {
+    auto go = [&](auto kern) {
+      kern<<<(unsigned)blocks, 256, 0, s>>>(v4(x), v4(y), seed ? v4(seed) : nullptr, pairs, wsum, out);
+    };
+    if (seed) {
+      if (words == 64) go(k_dot_fixed<1, true>);
+      else if (words == 128) go(k_dot_fixed<2, true>);
+      else go(k_dot_fixed<4, true>);
+    } else {
+      if (words == 64) go(k_dot_fixed<1, false>);
+      else if (words == 128) go(k_dot_fixed<2, false>);
+      else go(k_dot_fixed<4, false>);
+    }
+  } else if (vec && seed)
     k_dot_batched<true><<<(unsigned)blocks, 256, 0, s>>>(v4(x), v4(y), v4(seed), words, pairs, wsum, out);
   else if (vec)
     k_dot_batched<false><<<(unsigned)blocks, 256, 0, s>>>(v4(x), v4(y), nullptr, words, pairs, wsum, out);

@@ -140,7 +140,7 @@ def test_batched_dot_cfg1_vs_oracle(tk, oracle):
     assert np.array_equal(got[:64], (al * wl).sum(1))
 
 
-@pytest.mark.parametrize("words", [1, 2, 3, 7, 64, 128, 129, 300, 1000])
+@pytest.mark.parametrize("words", [1, 2, 3, 7, 64, 128, 129, 256, 300, 1000])
 def test_batched_dot_ragged_words_and_premask(tk, oracle, words):
     """Word counts around the kernel's 4 x 16 B per-lane chunks (odd counts
     take the u64 kernel), the cfg1 row (128) and rows longer than one chunk;
