@@ -389,13 +389,14 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
     // CH skip values (raw bits: f32, or the sign-extended s16 accumulator) of
     // one chunk; converted only where they are used, so the loads stay in flight
     auto load_skip = [&](long long base, uint32_t (&skr)[CH]) {
-      uint32_t off = 0;
       if (p.skip16) {
+        const int16_t* q = p.skip16 + base;
 #pragma unroll
-        for (int j = 0; j < CH; ++j, off += ostride) skr[j] = (uint32_t)(int32_t)__ldg(p.skip16 + base + off);
+        for (int j = 0; j < CH; ++j, q += ostride) skr[j] = (uint32_t)(int32_t)__ldg(q);
       } else {
+        const float* q = p.skip + base;
 #pragma unroll
-        for (int j = 0; j < CH; ++j, off += ostride) skr[j] = __float_as_uint(__ldg(p.skip + base + off));
+        for (int j = 0; j < CH; ++j, q += ostride) skr[j] = __float_as_uint(__ldg(q));
       }
     };
     uint32_t skr[CH];        // skip values of the next chunk to consume
@@ -442,9 +443,9 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
         if (pre && !skr_ready) load_skip(skb, skr);
         skr_ready = false;
       } else if (pre) {
-        uint32_t off = 0;
+        const float* q = p.skip + skb;
 #pragma unroll
-        for (int j = 0; j < CH; ++j, off += ostride) sk[j] = __ldg(p.skip + skb + off);
+        for (int j = 0; j < CH; ++j, q += ostride) sk[j] = __ldg(q);
       }
       if (TK_DBG(p.dbg) & 1024)
         sm100::mbar_wait(&a_full[acc], (it / kAcc) & 1);
@@ -503,8 +504,8 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
                 w[j] = b;
               }
             }
-            const int Rq = p.q_R[o];
-            const int chq = n0 / Rq, cq = n0 - chq * Rq;
+            const int Rq = p.q_R[o];  // 64 or 128: a shift, not a division
+            const int chq = Rq == 128 ? n0 >> 7 : n0 >> 6, cq = n0 - chq * Rq;
             const long long off = p.q_phases[o] == 4 ? ((long long)(chq * 4 + ph4) * p.q_pos[o] + P4) * Rq + cq
                                                      : ((long long)chq * p.q_pos[o] + P1) * Rq + cq;
             uint4* dst = reinterpret_cast<uint4*>(p.q[o] + off);
@@ -517,9 +518,8 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
         if constexpr (BN >= 128) {
           if (p.aout) {  // downsample: exact s16 accumulators (|acc| <= 2K < 2^15, host-checked)
             int16_t* ob = p.aout + fbase + (long long)n0 * oplane;
-            uint32_t off = 0;
 #pragma unroll
-            for (int j = 0; j < CH; ++j, off += ostride) ob[off] = (int16_t)(int32_t)r[j];
+            for (int j = 0; j < CH; ++j, ob += ostride) *ob = (int16_t)(int32_t)r[j];
             continue;
           }
         }
@@ -550,10 +550,10 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
 #pragma unroll
             for (int j = 0; j < CH; ++j) v[j] += sk[j];
             if (c0 + CH < BN) {
+              // pointer increments: one IMAD.WIDE per element (no 64-bit index math)
               const float* sb = p.skip + skb + (size_t)(c0 + CH) * ostride;
-              uint32_t off = 0;
 #pragma unroll
-              for (int j = 0; j < CH; ++j, off += ostride) sk[j] = __ldg(sb + off);
+              for (int j = 0; j < CH; ++j, sb += ostride) sk[j] = __ldg(sb);
             }
           }
         } else if (pre) {  // NCHW: lanes = consecutive positions -> coalesced per channel
@@ -592,17 +592,20 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
         }
         if (p.fout && !(TK_DBG(p.dbg) & 256)) {
           float* ob = p.fout + fbase + (long long)n0 * oplane;
-          uint32_t off = 0;
 #pragma unroll
-          for (int j = 0; j < CH; ++j, off += ostride) ob[off] = v[j];
+          for (int j = 0; j < CH; ++j, ob += ostride) *ob = v[j];
         }
         if (p.n_q > 0 && !(TK_DBG(p.dbg) & 128)) {
           // quantizer input checks (R:quantizer.hpp:37-41,53-55), once per
-          // value: after the ReLU a value is >= 0 (or -0.0) unless NaN
+          // value: after the ReLU a value is >= 0 (or -0.0) unless it is NaN
+          // or +inf, exactly the values for which v * 0 is NaN -- one FMA
+          // per value folds the check, one compare per chunk reads it
           bool bad = false;
           if (p.relu) {
+            float z = 0.0f;
 #pragma unroll
-            for (int j = 0; j < CH; ++j) bad |= !(v[j] <= 3.402823466e38f);
+            for (int j = 0; j < CH; ++j) z = __fmaf_rn(v[j], 0.0f, z);
+            bad = z != z;
           } else {
 #pragma unroll
             for (int j = 0; j < CH; ++j) bad |= !(v[j] >= 0.0f && v[j] <= 3.402823466e38f);
@@ -618,15 +621,16 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
               for (int j = 0; j < CH / 4; ++j) {
                 uint32_t b = 0;
 #pragma unroll
-                for (int i = 0; i < 4; ++i) {
+                for (int i = 0; i < 4; ++i) {  // level byte = (x > t0) + (x > t1): predicated adds
                   const float x = v[4 * j + i];
-                  b += ((x > t0) ? (1u << (8 * i)) : 0u) + ((x > t1) ? (1u << (8 * i)) : 0u);
+                  if (x > t0) b += 1u << (8 * i);
+                  if (x > t1) b += 1u << (8 * i);
                 }
                 w[j] = b;
               }
             }
-            const int Rq = p.q_R[o];
-            const int chq = n0 / Rq, cq = n0 - chq * Rq;
+            const int Rq = p.q_R[o];  // 64 or 128: a shift, not a division
+            const int chq = Rq == 128 ? n0 >> 7 : n0 >> 6, cq = n0 - chq * Rq;
             const long long off = p.q_phases[o] == 4 ? ((long long)(chq * 4 + ph4) * p.q_pos[o] + P4) * Rq + cq
                                                      : ((long long)chq * p.q_pos[o] + P1) * Rq + cq;
             uint4* dst = reinterpret_cast<uint4*>(p.q[o] + off);
