@@ -85,13 +85,21 @@ struct ConvK {
   float out_scale;
   int relu;
   int N;
-  const float* skip;  // NCHW
-  float* fout;        // NCHW
+  // Residual tensors inside the network are channel-blocked, [N][C/16][H*W][16]
+  // (element (n, c, p) at ((n * C/16 + c/16) * HW + p) * 16 + c % 16): a
+  // thread's 16-channel chunk is one (s16) or two (f32) 32-byte sectors moved
+  // by 256-bit accesses, and the 32 positions of a warp are contiguous, so
+  // stores write whole lines.  The forward's input x (an identity shortcut of
+  // the first block) and a conv2d_ternary plan's output are NCHW.
+  const float* skip;  // blocked (skip_cl) or NCHW
+  float* fout;        // blocked (fout_cl) or NCHW
+  int skip_cl, fout_cl;
+  int res16_cl;  // the s16 downsample residual (aout / skip16) channel-blocked, else NCHW
   // exact s16 residual of a downsample conv: that conv stores its integer
   // accumulators (aout) instead of f32 and the consumer recomputes the folded
   // BN, fmaf(sk_gain, sk_scale * acc, sk_bias) -- the same f32 bits, half the bytes
-  int16_t* aout;         // NCHW, downsample conv
-  const int16_t* skip16; // NCHW, the block's last conv
+  int16_t* aout;         // blocked (res16_cl) or NCHW, downsample conv
+  const int16_t* skip16; // blocked (res16_cl) or NCHW, the block's last conv
   const float* sk_gain;
   const float* sk_bias;
   float sk_scale;
@@ -378,21 +386,47 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
     const bool has_skip = (p.skip || (BN >= 128 && p.skip16)) && !(TK_DBG(p.dbg) & (4 | 512));
     // element offset of (item's first channel, this thread's position) in the
     // NCHW skip tensor, or -1 when the position is past the batch / padding
+    // channel-last skip (internal f32 or s16 residual): chunk c0 is at
+    // base + c0; NCHW (the forward's input): at base + c0 * plane
+    const bool skip_cl = p.skip16 ? p.res16_cl != 0 : p.skip_cl != 0;
+    const long long bstride = oplane * 16;  // elements per 16-channel block of an image
+    // offset of channel c (a multiple of 16) from channel 0 of a position
+    auto ch_off = [&](int c, bool cl) -> long long { return cl ? (long long)(c >> 4) * bstride : (long long)c * ostride; };
     auto skip_at = [&](int item) -> long long {
       const int mi = item / p.n_tiles, nt = item - mi * p.n_tiles;
       const int qrow = (mi * MT + grp % MT) * 128 + qtr * 32 + lane;
       const int img = qrow / plane, rem = qrow - img * plane;
       const int oy = rem / p.PWg, ox = rem - (rem / p.PWg) * p.PWg;
       if (!(qrow < p.m_total && oy < p.Ho && ox < p.Wo)) return -1;
+      if (skip_cl) return (long long)img * p.N * oplane + ((long long)oy * p.Wo + ox) * 16 + ch_off(nt * BN, true);
       return (long long)img * p.N * oplane + (long long)oy * p.Wo + ox + (long long)(nt * BN) * oplane;
     };
     // CH skip values (raw bits: f32, or the sign-extended s16 accumulator) of
     // one chunk; converted only where they are used, so the loads stay in flight
     auto load_skip = [&](long long base, uint32_t (&skr)[CH]) {
-      if (p.skip16) {
+      if (p.skip16 && !p.res16_cl) {
         const int16_t* q = p.skip16 + base;
 #pragma unroll
         for (int j = 0; j < CH; ++j, q += ostride) skr[j] = (uint32_t)(int32_t)__ldg(q);
+      } else if (p.skip16) {
+#pragma unroll
+        for (int h = 0; h < CH / 16; ++h) {
+          uint32_t w[8];
+          sm100::ld_nc_v8(p.skip16 + base + h * bstride, w);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            skr[16 * h + 2 * i] = (uint32_t)(int32_t)(int16_t)(w[i] & 0xFFFFu);
+            skr[16 * h + 2 * i + 1] = (uint32_t)((int32_t)w[i] >> 16);
+          }
+        }
+      } else if (p.skip_cl) {
+#pragma unroll
+        for (int h = 0; h < CH / 8; ++h) {
+          uint32_t w[8];
+          sm100::ld_nc_v8(p.skip + base + (h >> 1) * bstride + 8 * (h & 1), w);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) skr[8 * h + i] = w[i];
+        }
       } else {
         const float* q = p.skip + base;
 #pragma unroll
@@ -428,14 +462,16 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
       const int py = oy + 1, px = ox + 1;
       const long long P4 = ((long long)img * p.o_PH + (py >> 1)) * p.o_PW + (px >> 1);
       const int ph4 = (py & 1) * 2 + (px & 1);
-      // NCHW index of (img, channel 0, oy, ox) in the f32 skip / output tensors
+      // NCHW index of (img, channel 0, oy, ox) in the f32 skip / output tensors,
+      // and the channel-last one ((img, oy, ox) * C)
       const long long fbase = (long long)img * p.N * oplane + (long long)oy * p.Wo + ox;
+      const long long hbase = (long long)img * p.N * oplane + ((long long)oy * p.Wo + ox) * 16;
       // skip values are independent of the accumulator: the first chunk's
       // loads were issued during the previous item's last chunk (else here,
       // before waiting for the MMAs), each later chunk's while the previous
       // one is finished (HBM latency off the critical path)
       const bool pre = has_skip && valid;
-      const long long skb = fbase + (long long)(nt * BN) * oplane;
+      const long long skb = (skip_cl ? hbase : fbase) + ch_off(nt * BN, skip_cl);
       // BN = 64 kernels (576 threads at the register cap) keep the plain f32
       // form: measured faster than the raw-bit / one-item-ahead variant there
       float sk[CH];
@@ -443,9 +479,19 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
         if (pre && !skr_ready) load_skip(skb, skr);
         skr_ready = false;
       } else if (pre) {
-        const float* q = p.skip + skb;
+        if (p.skip_cl) {
 #pragma unroll
-        for (int j = 0; j < CH; ++j, q += ostride) sk[j] = __ldg(q);
+          for (int h = 0; h < CH / 8; ++h) {
+            uint32_t w[8];
+            sm100::ld_nc_v8(p.skip + skb + (h >> 1) * bstride + 8 * (h & 1), w);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) sk[8 * h + i] = __uint_as_float(w[i]);
+          }
+        } else {
+          const float* q = p.skip + skb;
+#pragma unroll
+          for (int j = 0; j < CH; ++j, q += ostride) sk[j] = __ldg(q);
+        }
       }
       if (TK_DBG(p.dbg) & 1024)
         sm100::mbar_wait(&a_full[acc], (it / kAcc) & 1);
@@ -517,9 +563,20 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
         if constexpr (MT >= 2) continue;  // MT > 1 kernels: integer epilogue only (host-checked)
         if constexpr (BN >= 128) {
           if (p.aout) {  // downsample: exact s16 accumulators (|acc| <= 2K < 2^15, host-checked)
-            int16_t* ob = p.aout + fbase + (long long)n0 * oplane;
+            if (p.res16_cl) {
+              int16_t* ob = p.aout + hbase + ch_off(n0, true);  // blocked: one 32-byte store per 16 channels
 #pragma unroll
-            for (int j = 0; j < CH; ++j, ob += ostride) *ob = (int16_t)(int32_t)r[j];
+              for (int h = 0; h < CH / 16; ++h) {
+                uint32_t w[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) w[i] = (r[16 * h + 2 * i] & 0xFFFFu) | (r[16 * h + 2 * i + 1] << 16);
+                sm100::st_v8(ob + h * bstride, w);
+              }
+            } else {
+              int16_t* ob = p.aout + fbase + (long long)n0 * oplane;
+#pragma unroll
+              for (int j = 0; j < CH; ++j, ob += ostride) *ob = (int16_t)(int32_t)r[j];
+            }
             continue;
           }
         }
@@ -550,10 +607,20 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
 #pragma unroll
             for (int j = 0; j < CH; ++j) v[j] += sk[j];
             if (c0 + CH < BN) {
-              // pointer increments: one IMAD.WIDE per element (no 64-bit index math)
-              const float* sb = p.skip + skb + (size_t)(c0 + CH) * ostride;
+              if (p.skip_cl) {
 #pragma unroll
-              for (int j = 0; j < CH; ++j, sb += ostride) sk[j] = __ldg(sb);
+                for (int h = 0; h < CH / 8; ++h) {
+                  uint32_t w[8];
+                  sm100::ld_nc_v8(p.skip + skb + ch_off(c0 + CH, true) + (h >> 1) * bstride + 8 * (h & 1), w);
+#pragma unroll
+                  for (int i = 0; i < 8; ++i) sk[8 * h + i] = __uint_as_float(w[i]);
+                }
+              } else {
+                // pointer increments: one IMAD.WIDE per element (no 64-bit index math)
+                const float* sb = p.skip + skb + (size_t)(c0 + CH) * ostride;
+#pragma unroll
+                for (int j = 0; j < CH; ++j, sb += ostride) sk[j] = __ldg(sb);
+              }
             }
           }
         } else if (pre) {  // NCHW: lanes = consecutive positions -> coalesced per channel
@@ -573,7 +640,7 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
             for (int j = 0; j < CH; ++j) v[j] += __uint_as_float(skr[j]);
           }
           if (c0 + CH < BN) {
-            load_skip(skb + (long long)(c0 + CH) * ostride, skr);
+            load_skip(skb + ch_off(c0 + CH, skip_cl), skr);
           } else {
             // last chunk: this group's next item's first chunk, one item ahead
             const int nxt = item + (G / MT) * (int)gridDim.x;
@@ -591,9 +658,20 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
           for (int j = 0; j < CH; ++j) v[j] = v[j] < 0.0f ? 0.0f : v[j];  // std::max(v, 0.0f)
         }
         if (p.fout && !(TK_DBG(p.dbg) & 256)) {
-          float* ob = p.fout + fbase + (long long)n0 * oplane;
+          if (p.fout_cl) {  // blocked: two 32-byte stores per 16 channels
+            float* ob = p.fout + hbase + ch_off(n0, true);
 #pragma unroll
-          for (int j = 0; j < CH; ++j, ob += ostride) *ob = v[j];
+            for (int h = 0; h < CH / 8; ++h) {
+              uint32_t w[8];
+#pragma unroll
+              for (int i = 0; i < 8; ++i) w[i] = __float_as_uint(v[8 * h + i]);
+              sm100::st_v8(ob + (h >> 1) * bstride + 8 * (h & 1), w);
+            }
+          } else {
+            float* ob = p.fout + fbase + (long long)n0 * oplane;
+#pragma unroll
+            for (int j = 0; j < CH; ++j, ob += ostride) *ob = v[j];
+          }
         }
         if (p.n_q > 0 && !(TK_DBG(p.dbg) & 128)) {
           // quantizer input checks (R:quantizer.hpp:37-41,53-55), once per
@@ -1017,6 +1095,39 @@ __global__ void __launch_bounds__(64) k_pool_nchw(const float* __restrict__ x, i
   out[p0 + threadIdx.x] = s / (float)HW;
 }
 
+// the same mean over a channel-blocked [N][C/16][HW][16] tensor: a thread
+// per (n, c) sums its positions left to right (the reference's order); the
+// 16 channels of a block are 64 contiguous bytes per position
+__global__ void __launch_bounds__(256) k_pool_cb16(const float* __restrict__ x, int N, int HW, int C,
+                                                   float* __restrict__ out) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= (long long)N * C) return;
+  const long long n = i / C;
+  const int c = (int)(i - n * C);
+  const float* q = x + (n * C + (c & ~15)) * HW + (c & 15);
+  float s = 0.0f;
+  for (int j = 0; j < HW; ++j, q += 16) s += __ldg(q);
+  out[i] = s / (float)HW;
+}
+
+// channel-blocked [N][C/16][HW][16] -> NCHW (the body output the caller asked for)
+__global__ void __launch_bounds__(256) k_cb16_to_nchw(const float* __restrict__ x, int N, int HW, int C,
+                                                      float* __restrict__ out) {
+  const long long total = (long long)N * C * HW;
+  for (long long o = blockIdx.x * (long long)blockDim.x + threadIdx.x; o < total;
+       o += (long long)gridDim.x * blockDim.x) {
+    const long long n = o / ((long long)C * HW);
+    const long long r = o - n * C * HW;
+    const int c = (int)(r / HW), p = (int)(r - (long long)c * HW);
+    out[o] = __ldg(x + (n * C + (c & ~15)) * HW + (long long)p * 16 + (c & 15));
+  }
+}
+
+void pool_cb16(const float* x, int N, int HW, int C, float* out, cudaStream_t s) {
+  const long long nc = (long long)N * C;
+  k_pool_cb16<<<(unsigned)((nc + 255) / 256), 256, 0, s>>>(x, N, HW, C, out);
+}
+
 void pool_nchw(const float* x, int NC, int HW, float* out, cudaStream_t s) {
   // planes per block: up to 64, within 96 KB of staged floats
   const int planes = std::max(1, std::min(64, (96 * 1024) / (HW * 4)));
@@ -1118,6 +1229,7 @@ struct tk_net {
   tk_context* ctx = nullptr;
   int fused = 0;
   int single = 0;  // one conv, no residual (conv2d_ternary plan, tk_fconv_run)
+  int f32_cl = 1;  // internal f32 residual tensors channel-blocked [N][C/16][HW][16], not NCHW
   int batch = 0, in_c = 0, in_h = 0, in_w = 0;
   int out_c = 0, out_h = 0, out_w = 0;
   std::vector<tk_block_desc> blocks;
@@ -1375,6 +1487,7 @@ int setup_fused(tk_net* net) {
 // fused plan (net->convs); pack_a / pack_b: the s8 tensors the input is
 // quantized into (pack_b may be -1).
 int finish_fused(tk_net* net, int pack_a, int pack_b) {
+  net->f32_cl = tk_knob("TK_NET_F32_NCHW", 0) ? 0 : 1;
   // allocate tensors
   for (auto& t : net->s8) {
     if (cudaMalloc(&t.p, t.bytes()) != cudaSuccess) return TK_ERR_CUDA;
@@ -1446,6 +1559,14 @@ int finish_fused(tk_net* net, int pack_a, int pack_b) {
       k.o_PH = k.o_Hp / 2; k.o_PW = k.o_Wp / 2;
       k.skip = cv.skip_f >= 0 ? net->f32[cv.skip_f].p : nullptr;  // -2: patched at launch
       k.fout = cv.out_f >= 0 ? net->f32[cv.out_f].p : nullptr;
+      // the network's own residual tensors are channel-last; x and a plan's
+      // caller output (-2 / -3) are NCHW
+      k.skip_cl = cv.skip_f >= 0 && net->f32_cl ? 1 : 0;
+      k.fout_cl = cv.out_f >= 0 && net->f32_cl ? 1 : 0;
+      // (measured, tools/layer_ab.py: the f32 residual channel-blocked is 4-10%
+      // faster per body than NCHW; the s16 one is not -- its blocked stores
+      // are faster in the downsample convs but its readers slower overall)
+      k.res16_cl = tk_knob("TK_NET_S16_CB16", 0) ? 1 : 0;
       k.aout = nullptr;
       k.skip16 = nullptr;
       k.sk_gain = k.sk_bias = nullptr;
@@ -1845,8 +1966,14 @@ int tk_net_forward(tk_context* ctx, tk_net* net, const float* x, float* out, flo
         ++ci;
       }
     const F32T& f = net->f32[net->final_f];
-    if (out) cudaMemcpyAsync(out, f.p, (size_t)f.elems * 4, cudaMemcpyDeviceToDevice, s);
-    if (pooled)
+    if (out && net->f32_cl)
+      k_cb16_to_nchw<<<(unsigned)std::min<long long>((f.elems + 255) / 256, 148 * 32), 256, 0, s>>>(
+          f.p, net->batch, f.H * f.W, f.C, out);
+    else if (out)
+      cudaMemcpyAsync(out, f.p, (size_t)f.elems * 4, cudaMemcpyDeviceToDevice, s);
+    if (pooled && net->f32_cl)
+      pool_cb16(f.p, net->batch, f.H * f.W, f.C, pooled, s);
+    else if (pooled)
       pool_nchw(f.p, net->batch * f.C, f.H * f.W, pooled, s);
     return cudaGetLastError() == cudaSuccess ? TK_OK : TK_ERR_CUDA;
   }
