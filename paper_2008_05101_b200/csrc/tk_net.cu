@@ -1328,12 +1328,13 @@ void plan_taps(Conv& cv, const S8T& in) {
   k.Wo = conv_out(in.W, d);
 }
 
-int prepare_conv_weights(Conv& cv, int R) {
+// bn: N tile width (0 = the default: the whole layer up to 256 channels)
+int prepare_conv_weights(Conv& cv, int R, int bn) {
   const tk_conv_desc& d = cv.d;
   const int taps = d.k * d.k, chunks = d.in_c / R;
   cv.R = R;
   cv.chunks = chunks;
-  cv.BN = d.out_c >= 256 ? 256 : d.out_c;  // 64, 128, 256
+  cv.BN = bn ? bn : (d.out_c >= 256 ? 256 : d.out_c);  // 64, 128, 256
   if (const int bnmax = tk_knob("TK_CONV_BNMAX", 0)) cv.BN = std::min(cv.BN, std::max(64, bnmax));
   cv.n_tiles = d.out_c / cv.BN;
   const size_t blk = (size_t)cv.BN * R;
@@ -1501,7 +1502,19 @@ int finish_fused(tk_net* net, int pack_a, int pack_b) {
     for (auto& cv : cvs) {
       ++conv_no;
       const S8T& in = net->s8[cv.in_idx];
-      int st = prepare_conv_weights(cv, in.R);
+      // integer-threshold (inner) convs: ReLU + quantize only, no floats out
+      bool inner = cv.relu && cv.skip_f == -1 && cv.out_f < 0 && cv.q_idx[0] >= 0;
+      if (inner) {
+        tk_qparams q0;
+        const S8T& q = net->s8[cv.q_idx[0]];
+        inner = tk_make_qparams(q.ta1, q.ta2, TK_MODE_ACTIVATION_NONNEG, &q0) == TK_OK && q0.t0 >= 0.0f;
+      }
+      // wide inner convs (>= 256 channels, weights streamed per item): 128-wide
+      // N tiles with two M tiles per item, so every streamed weight block
+      // serves 256 positions (half the weight bytes per MAC of a 256-wide
+      // single tile)
+      const bool wide_mt2 = inner && cv.d.out_c >= 256 && tk_knob("TK_CONV_WIDE_MT2", 1);
+      int st = prepare_conv_weights(cv, in.R, wide_mt2 ? 128 : 0);
       if (st != TK_OK) return st;
       plan_taps(cv, in);
       ConvK& k = cv.k;
@@ -1513,16 +1526,9 @@ int finish_fused(tk_net* net, int pack_a, int pack_b) {
       // (measured: pays off for the 64-channel inner convs; the f32-epilogue
       // convs and wider layers run faster with the two epilogue groups on
       // alternate items)
-      // integer-threshold (inner) convs: ReLU + quantize only, no floats out
-      bool inner = cv.relu && cv.skip_f == -1 && cv.out_f < 0 && cv.q_idx[0] >= 0;
-      if (inner) {
-        tk_qparams q0;
-        const S8T& q = net->s8[cv.q_idx[0]];
-        inner = tk_make_qparams(q.ta1, q.ta2, TK_MODE_ACTIVATION_NONNEG, &q0) == TK_OK && q0.t0 >= 0.0f;
-      }
       // (MT > 1 kernels carry the integer epilogue only)
       // (MT = 4 measured no faster than 2 on the ResNet-18 stage-1 convs)
-      cv.MT = (cv.BN == 64 && inner && k.m_tiles > 1) ? 2 : 1;
+      cv.MT = ((cv.BN == 64 || wide_mt2) && inner && k.m_tiles > 1) ? 2 : 1;
       if (const int mt = tk_knob("TK_CONV_MT", 0)) cv.MT = std::min(cv.MT, std::max(1, mt));
       k.m_items = (k.m_tiles + cv.MT - 1) / cv.MT;
       {
@@ -1704,6 +1710,9 @@ template <int BN, int R, int KT>
 cudaError_t launch_conv_mt(const Conv& cv, const float* x, float* out, int pdl, cudaStream_t s) {
   if constexpr (BN == 64) {
     if (cv.MT == 4) return launch_conv<BN, R, KT, 4>(cv, x, out, pdl, s);
+    if (cv.MT == 2) return launch_conv<BN, R, KT, 2>(cv, x, out, pdl, s);
+  }
+  if constexpr (BN == 128) {
     if (cv.MT == 2) return launch_conv<BN, R, KT, 2>(cv, x, out, pdl, s);
   }
   return launch_conv<BN, R, KT, 1>(cv, x, out, pdl, s);
