@@ -1,10 +1,10 @@
 """Turn the raw outputs of tools/profile_round.sh (gpurun_out/prof/) into the
 tracked summaries under profiles/:
 
-* bench_r01_<workload>.json      -- the bench line of each workload
-* ncu_launches_r01_resnet18.{csv,txt} -- launch list of the default bench command
-* traffic_r01.json               -- DRAM bytes per launch of each dominant kernel
-* ncu_full_r01_<name>.txt        -- key metrics of each `ncu --set full` capture
+* bench_r02_<workload>.json      -- the bench line of each workload
+* ncu_launches_r02_resnet18.{csv,txt} -- launch list of the default bench command
+* traffic_r02.json               -- DRAM bytes per launch of each dominant kernel
+* ncu_full_r02_<name>.txt        -- key metrics of each `ncu --set full` capture
 
 Run here (ncu -i reads the .ncu-rep files without a GPU)."""
 import csv
@@ -44,7 +44,12 @@ def bench_lines():
             continue
         lines = [ln for ln in open(p).read().splitlines() if ln.startswith("{")]
         if lines:
-            with open(os.path.join(OUT, f"bench_r01_{w}.json"), "w") as f:
+            with open(os.path.join(OUT, f"bench_r02_{w}.json"), "w") as f:
+                f.write(lines[-1] + "\n")
+        p = os.path.join(RAW, f"ref_{w}.json")
+        lines = [ln for ln in open(p).read().splitlines() if ln.startswith("{")] if os.path.exists(p) else []
+        if lines:
+            with open(os.path.join(OUT, f"bench_r02_reference_{w}.json"), "w") as f:
                 f.write(lines[-1] + "\n")
             print("bench", w, json.loads(lines[-1])["value"])
 
@@ -54,9 +59,9 @@ def launches():
     if not os.path.exists(p):
         return
     ls = per_launch(p)
-    with open(os.path.join(OUT, "ncu_launches_r01_resnet18.csv"), "w") as f:
+    with open(os.path.join(OUT, "ncu_launches_r02_resnet18.csv"), "w") as f:
         f.write(open(p).read())
-    with open(os.path.join(OUT, "ncu_launches_r01_resnet18.txt"), "w") as f:
+    with open(os.path.join(OUT, "ncu_launches_r02_resnet18.txt"), "w") as f:
         f.write("ncu --metrics gpu__time_duration.sum --clock-control none: python bench.py --steps 3 --warmup 3\n")
         f.write("(serialised, cold-cache per-launch times; shares, not absolutes, compare with the bench)\n\n")
         tot = {}
@@ -74,8 +79,8 @@ def launches():
 
 
 def traffic():
-    path = os.path.join(OUT, "traffic_r01.json")
-    old = json.load(open(path)) if os.path.exists(path) else {}
+    path = os.path.join(OUT, "traffic_r02.json")
+    old = {}
     specs = {"resnet18": 256, "resnet50": 128, "fc": None, "dot": None}
     for w, batch in specs.items():
         p = os.path.join(RAW, f"traffic_{w}.csv")
@@ -117,7 +122,7 @@ def full(name, rep, note):
                           "sm__inst_executed_pipe_tc.avg.pct_of_peak_sustained_active,"
                           "sm__pipe_tc_cycles_active.avg.pct_of_peak_sustained_active"],
                          capture_output=True, text=True).stdout
-    with open(os.path.join(OUT, f"ncu_full_r01_{name}.txt"), "w") as f:
+    with open(os.path.join(OUT, f"ncu_full_r02_{name}.txt"), "w") as f:
         f.write(note + "\n\n")
         f.write(f"kernel: {rows[1][ik]}\n")
         seen = set()
@@ -143,13 +148,10 @@ def main():
     traffic()
     full("r18_conv1", "full_r18_conv1.ncu-rep",
          "ncu --set full --clock-control none -k regex:k_conv_tc -s 1 -c 1 python tools/prof_net.py\n"
-         "(ResNet-18 b256, second conv launch = stage-1 block-1 conv2: 3x3 64->64, f32 skip add, f32 + s8 out)")
+         "(ResNet-18 b256, second conv launch = stage-1 block-0 conv2: 3x3 64->64, f32 skip add (x, NCHW), f32 (channel-blocked) + s8 out)")
     full("fc_gemm", "full_fc_gemm.ncu-rep",
          "BACKEND=TC_F4 ncu --set full --clock-control none -k regex:k_gemm_tc -s 2 -c 1 python tools/prof_fc.py\n"
          "(cfg3 FC 4096x4096 b256, FP4 pipe, int32 out, tile chosen by the launcher; ncu flushes caches)")
-    full("stem", "full_stem.ncu-rep",
-         "B=64 ncu --set full --clock-control none -k regex:k_stem_conv -c 1 python tools/stem_split.py\n"
-         "(fp32 7x7/2 stem convolution of the e2e path, 64 images)")
 
 
 if __name__ == "__main__":
