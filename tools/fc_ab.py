@@ -33,10 +33,12 @@ def main():
                                tk.layer_k_pad(layer, fmt), fmt)
         out = torch.empty((B, N), dtype=torch.float32, device="cuda")
         configs = [("auto", {})]
-        for bn, sp in ((128, 1), (128, 2), (256, 2), (256, 4), (64, 2)):
+        for mc in (2, 4, 8):
+            configs.append((f"A multicast x{mc}", {"TK_GEMM_MC": str(mc)}))
+        for bn, sp in [tuple(map(int, c.split("x"))) for c in os.environ.get("FC_TILES", "").split(",") if c]:
             configs.append((f"BN{bn} S{sp}", {"TK_GEMM_BN": str(bn), "TK_GEMM_SPLIT": str(sp)}))
         for kern, env in configs:
-            for k in ("TK_GEMM_BN", "TK_GEMM_SPLIT"):
+            for k in ("TK_GEMM_BN", "TK_GEMM_SPLIT", "TK_GEMM_MC"):
                 os.environ.pop(k, None)
             os.environ.update(env)
             for _ in range(3):
