@@ -47,17 +47,22 @@ namespace {
 // epilogue walks the accumulator row 16 columns at a time (<= 128 registers).
 // (a group waits on accumulator-buffer parity, so groups <= buffers: with
 // at most one pass of lead no waiter can match a stale phase)
-__host__ __device__ constexpr int conv_groups(int BN, int MT) {
-  return MT >= 2 ? 4 : (BN == 64 ? 4 : (BN <= 128 ? 3 : 2));
+// GPI (column split): a BN = 256 single-tile item may be shared by two groups,
+// each taking half its columns, so 16 epilogue warps (not 8) keep skip loads
+// and stores in flight on the wide f32-epilogue layers (chosen per conv, §4.6)
+__host__ __device__ constexpr int conv_groups(int BN, int MT, int GPI = 1) {
+  return MT >= 2 ? 4 : (BN == 64 ? 4 : (BN <= 128 ? 3 : 2 * GPI));
 }
-__host__ __device__ constexpr int conv_threads(int BN, int MT) { return 64 + 128 * conv_groups(BN, MT); }
+__host__ __device__ constexpr int conv_threads(int BN, int MT, int GPI = 1) {
+  return 64 + 128 * conv_groups(BN, MT, GPI);
+}
 // accumulator columns per epilogue step: 16 keeps 3-4 groups within 128 /
 // 96 registers; with 2 groups (168 registers) 32 columns double the f32
 // skip loads in flight per thread (the wide 1x1 f32-epilogue layers of
 // ResNet-50 are HBM-latency bound)
 // (measured: pays off on the 1x1 layers; the 3x3 ones spill)
-__host__ __device__ constexpr int conv_chunk(int BN, int MT, int KT) {
-  return conv_groups(BN, MT) == 2 && KT == 1 ? 32 : 16;
+__host__ __device__ constexpr int conv_chunk(int BN, int MT, int KT, int GPI = 1) {
+  return conv_groups(BN, MT, GPI) == 2 && KT == 1 ? 32 : 16;
 }
 
 struct ConvK {
@@ -151,8 +156,8 @@ struct Acc {
   static constexpr uint32_t kCols = kN * BN * MT;    // TMEM columns (power of 2)
 };
 
-template <int BN, int R, int KT, int MT>
-__global__ void __launch_bounds__(conv_threads(BN, MT), 1)
+template <int BN, int R, int KT, int MT, int GPI>
+__global__ void __launch_bounds__(conv_threads(BN, MT, GPI), 1)
 k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CUtensorMap w_map,
           const ConvK p) {
   constexpr int kAcc = Acc<BN, MT>::kN;
@@ -206,7 +211,7 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
     }
     for (int s = 0; s < kAcc; ++s) {
       sm100::mbar_init(&a_full[s], 1);
-      sm100::mbar_init(&a_empty[s], 128 * MT);  // one epilogue group per M tile
+      sm100::mbar_init(&a_empty[s], 128 * MT * GPI);  // the groups sharing an item
     }
     sm100::mbar_init(w_res, 1);
 #pragma unroll
@@ -359,12 +364,14 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
     // G groups of 4 warps take turns on items (several items in flight hide
     // the TMEM-load and memory latencies); within a group warp w owns TMEM
     // lane quarter w % 4 and walks all BN columns.
-    constexpr int G = conv_groups(BN, MT), kEpiThreads = 128 * G;
-    constexpr int CH = conv_chunk(BN, MT, KT);
-    static_assert(G / MT <= kAcc, "epilogue groups must not outnumber accumulator buffers");
+    constexpr int G = conv_groups(BN, MT, GPI), kEpiThreads = 128 * G;
+    constexpr int CH = conv_chunk(BN, MT, KT, GPI);
+    constexpr int IG = G / GPI, BNG = BN / GPI;  // item groups, columns per group
+    static_assert(IG / MT <= kAcc, "epilogue groups must not outnumber accumulator buffers");
     const int et = threadIdx.x - 64;
     const int qtr = warp & 3;
     const int grp = (warp - 2) >> 2;
+    const int igrp = grp / GPI, half = grp % GPI;  // item-slot group, column part
     const int plane = p.PHg * p.PWg;
     const long long oplane = (long long)p.Ho * p.Wo;
     if constexpr (BN >= 128) {
@@ -394,12 +401,13 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
     auto ch_off = [&](int c, bool cl) -> long long { return cl ? (long long)(c >> 4) * bstride : (long long)c * ostride; };
     auto skip_at = [&](int item) -> long long {
       const int mi = item / p.n_tiles, nt = item - mi * p.n_tiles;
-      const int qrow = (mi * MT + grp % MT) * 128 + qtr * 32 + lane;
+      const int qrow = (mi * MT + igrp % MT) * 128 + qtr * 32 + lane;
       const int img = qrow / plane, rem = qrow - img * plane;
       const int oy = rem / p.PWg, ox = rem - (rem / p.PWg) * p.PWg;
       if (!(qrow < p.m_total && oy < p.Ho && ox < p.Wo)) return -1;
-      if (skip_cl) return (long long)img * p.N * oplane + ((long long)oy * p.Wo + ox) * 16 + ch_off(nt * BN, true);
-      return (long long)img * p.N * oplane + (long long)oy * p.Wo + ox + (long long)(nt * BN) * oplane;
+      if (skip_cl)
+        return (long long)img * p.N * oplane + ((long long)oy * p.Wo + ox) * 16 + ch_off(nt * BN + half * BNG, true);
+      return (long long)img * p.N * oplane + (long long)oy * p.Wo + ox + (long long)(nt * BN + half * BNG) * oplane;
     };
     // CH skip values (raw bits: f32, or the sign-extended s16 accumulator) of
     // one chunk; converted only where they are used, so the loads stay in flight
@@ -439,10 +447,10 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
     for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
       // MT == 1: the groups take turns on items; MT > 1: group g takes M tile
       // g % MT of every (G/MT)-th item
-      if (it % (G / MT) != grp / MT) continue;
+      if (it % (IG / MT) != igrp / MT) continue;
       const int mi = item / p.n_tiles, nt = item - mi * p.n_tiles;
-      const int mt = mi * MT + grp % MT;
-      const uint32_t tcol = (uint32_t)(it % kAcc) * (BN * MT) + (grp % MT) * BN;
+      const int mt = mi * MT + igrp % MT;
+      const uint32_t tcol = (uint32_t)(it % kAcc) * (BN * MT) + (igrp % MT) * BN + half * BNG;
       const int acc = it % kAcc;
       if (TK_DBG(p.dbg) & 8) {  // profiling: bare accumulator hand-off
         if (!(TK_DBG(p.dbg) & 64) || lane == 0) sm100::mbar_wait(&a_full[acc], (it / kAcc) & 1);
@@ -471,7 +479,7 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
       // before waiting for the MMAs), each later chunk's while the previous
       // one is finished (HBM latency off the critical path)
       const bool pre = has_skip && valid;
-      const long long skb = (skip_cl ? hbase : fbase) + ch_off(nt * BN, skip_cl);
+      const long long skb = (skip_cl ? hbase : fbase) + ch_off(nt * BN + half * BNG, skip_cl);
       // BN = 64 kernels (576 threads at the register cap) keep the plain f32
       // form: measured faster than the raw-bit / one-item-ahead variant there
       float sk[CH];
@@ -499,7 +507,7 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
         sm100::mbar_wait_sleep(&a_full[acc], (it / kAcc) & 1, 2000);
       sm100::tc_fence_after();
 #pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += CH) {
+      for (int c0 = 0; c0 < BNG; c0 += CH) {
         uint32_t r[CH];
         if constexpr (CH == 32)
           sm100::tmem_ld32(tmem + ((uint32_t)(qtr * 32) << 16) + tcol + c0, r);
@@ -507,7 +515,7 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
           sm100::tmem_ld16(tmem + ((uint32_t)(qtr * 32) << 16) + tcol + c0, r);
         sm100::tmem_ld_wait();
         if (!valid || (TK_DBG(p.dbg) & 4)) continue;
-        const int n0 = nt * BN + c0;
+        const int n0 = nt * BN + half * BNG + c0;
         if (p.ithr) {
           // integer-threshold epilogue: level = (s*acc > c0) + (s*acc > c1)
 #pragma unroll
@@ -606,7 +614,7 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
           if (pre) {  // NCHW: lanes = consecutive positions -> coalesced per channel
 #pragma unroll
             for (int j = 0; j < CH; ++j) v[j] += sk[j];
-            if (c0 + CH < BN) {
+            if (c0 + CH < BNG) {
               if (p.skip_cl) {
 #pragma unroll
                 for (int h = 0; h < CH / 8; ++h) {
@@ -639,11 +647,11 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
 #pragma unroll
             for (int j = 0; j < CH; ++j) v[j] += __uint_as_float(skr[j]);
           }
-          if (c0 + CH < BN) {
+          if (c0 + CH < BNG) {
             load_skip(skb + ch_off(c0 + CH, skip_cl), skr);
           } else {
             // last chunk: this group's next item's first chunk, one item ahead
-            const int nxt = item + (G / MT) * (int)gridDim.x;
+            const int nxt = item + (IG / MT) * (int)gridDim.x;
             if (nxt < n_items) {
               const long long nb = skip_at(nxt);
               if (nb >= 0) {
@@ -1213,6 +1221,7 @@ struct Conv {
   int smem = 0;
   int grid = 0;
   int MT = 1;  // 128-row M tiles per work item
+  int GPI = 1;  // epilogue groups sharing one item (column split, BN = 256 only)
 };
 
 
@@ -1610,6 +1619,10 @@ int finish_fused(tk_net* net, int pack_a, int pack_b) {
         ++k.n_q;
       }
       k.q_same = k.n_q == 2 && k.t0[0] == k.t0[1] && k.t1[0] == k.t1[1];
+      // column split for the wide f32-epilogue convs (measured, tools/layer_ab.py:
+      // -6..-19% on the skip + f32-output layers, but slower for the s16
+      // downsample output and for two next-layer quantizers)
+      cv.GPI = (cv.BN == 256 && cv.MT == 1 && !k.aout && k.n_q < 2 && tk_knob("TK_CONV_GPI", 1)) ? 2 : 1;
       // integer-threshold epilogue for inner convs (ReLU + quantize only)
       k.ithr = nullptr;
       k.ithr16 = 0;
@@ -1681,10 +1694,10 @@ int finish_fused(tk_net* net, int pack_a, int pack_b) {
   return TK_OK;
 }
 
-template <int BN, int R, int KT, int MT>
+template <int BN, int R, int KT, int MT, int GPI = 1>
 cudaError_t launch_conv(const Conv& cv, const float* x, float* out, int pdl, cudaStream_t s) {
   // 227 KB per block, less the kernel's static shared tables
-  if (const cudaError_t e = tk_smem_attr((const void*)k_conv_tc<BN, R, KT, MT>, 226 * 1024); e != cudaSuccess)
+  if (const cudaError_t e = tk_smem_attr((const void*)k_conv_tc<BN, R, KT, MT, GPI>, 226 * 1024); e != cudaSuccess)
     return e;
   ConvK k = cv.k;
   if (cv.skip_f == -2) k.skip = x;  // identity shortcut = the forward's input
@@ -1695,7 +1708,7 @@ cudaError_t launch_conv(const Conv& cv, const float* x, float* out, int pdl, cud
   // off (measured); on for conv2d_ternary plans, behind the input packing.
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(cv.grid);
-  cfg.blockDim = dim3(conv_threads(BN, MT));
+  cfg.blockDim = dim3(conv_threads(BN, MT, GPI));
   cfg.dynamicSmemBytes = cv.smem;
   cfg.stream = s;
   cudaLaunchAttribute at[1];
@@ -1703,7 +1716,7 @@ cudaError_t launch_conv(const Conv& cv, const float* x, float* out, int pdl, cud
   at[0].val.programmaticStreamSerializationAllowed = pdl;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, k_conv_tc<BN, R, KT, MT>, cv.in_map, cv.w_map, k);
+  return cudaLaunchKernelEx(&cfg, k_conv_tc<BN, R, KT, MT, GPI>, cv.in_map, cv.w_map, k);
 }
 
 template <int BN, int R, int KT>
@@ -1714,6 +1727,9 @@ cudaError_t launch_conv_mt(const Conv& cv, const float* x, float* out, int pdl, 
   }
   if constexpr (BN == 128) {
     if (cv.MT == 2) return launch_conv<BN, R, KT, 2>(cv, x, out, pdl, s);
+  }
+  if constexpr (BN == 256) {
+    if (cv.GPI == 2) return launch_conv<BN, R, KT, 1, 2>(cv, x, out, pdl, s);
   }
   return launch_conv<BN, R, KT, 1>(cv, x, out, pdl, s);
 }
