@@ -1522,7 +1522,10 @@ int finish_fused(tk_net* net, int pack_a, int pack_b) {
       // N tiles with two M tiles per item, so every streamed weight block
       // serves 256 positions (half the weight bytes per MAC of a 256-wide
       // single tile)
-      const bool wide_mt2 = inner && cv.d.out_c >= 256 && tk_knob("TK_CONV_WIDE_MT2", 1);
+      // (measured, tools/layer_ab.py: also pays off for 128-channel stride-2
+      // inner convs, not for 128-channel stride-1 ones)
+      const bool wide_mt2 = inner && (cv.d.out_c >= 256 || (cv.d.out_c >= 128 && cv.d.stride == 2)) &&
+                            tk_knob("TK_CONV_WIDE_MT2", 1);
       int st = prepare_conv_weights(cv, in.R, wide_mt2 ? 128 : 0);
       if (st != TK_OK) return st;
       plan_taps(cv, in);
