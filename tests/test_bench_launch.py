@@ -47,3 +47,16 @@ def test_world_size_mismatch_is_an_error():
 def test_single_gpu_is_not_relaunched():
     d = _line(_bench("--gpus", "1", "--dry-run", "--workload", "resnet18"))
     assert d["n_gpus"] == 1 and d["shards"] == [[0, 256]]
+
+
+def test_reference_arm_line():
+    """--impl reference: the reference's own CPU code (oracle/_ref) on the
+    workload, one JSON line with impl/value/unit/cpu_baseline/e2e (cfg2, the
+    cheapest workload; needs the reference build, made by build())."""
+    from oracle.oracle import reference_lib_path
+    if reference_lib_path() is None:
+        pytest.skip("oracle/_ref not built on this host")
+    d = _line(_bench("--impl", "reference", "--workload", "conv", "--steps", "2", "--warmup", "1", timeout=600))
+    assert d["impl"] == "reference" and d["unit"] == "Tops/s" and d["value"] > 0
+    assert d["cpu_baseline"]["kind"] == "reference" and d["cpu_baseline"]["cores"] >= 1
+    assert d["e2e"]["value"] == d["value"] and d["e2e"]["h2d_bytes_per_step"] == 0
