@@ -216,6 +216,11 @@ int tk_multibit_dot_batched(tk_context* ctx, const uint64_t* x_planes, int m, co
  * bias may be NULL. */
 int tk_matmul_t(tk_context* ctx, const float* x, const float* w, const float* bias, int batch, int in_dim,
                 int out_dim, int relu, float* y, void* stream);
+/* Dense fp32 layer of the ResNet head (outside the ternary path):
+ * y[b][o] = bias[o] + sum_k x[b][k] * w[o][k], one fp32 FMA chain in k order
+ * per output; w row-major [out_dim][in_dim], bias may be NULL. */
+int tk_dense_f32(tk_context* ctx, const float* x, const float* w, const float* bias, int batch, int in_dim,
+                 int out_dim, float* y, void* stream);
 /* packed_forward's block tail (R:tinynet.hpp:720-730): z[i] = max(z[i] + id, 0)
  * with id = fmaf(cal_gain[j], h[i], cal_bias[j]) (calibration present) or
  * h[i], j = i % hidden; both calibration pointers or neither. */

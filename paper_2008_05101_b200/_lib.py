@@ -75,6 +75,7 @@ SIGNATURES = {
     "tk_net_forward": (_i, [_vp, _vp, _vp, _vp, _vp, _vp]),
     "tk_affine_relu_maxpool": (_i, [_vp, _vp] + [_i] * 4 + [_vp, _vp, _vp, _vp]),
     "tk_matmul_t": (_i, [_vp, _vp, _vp, _vp, _i, _i, _i, _i, _vp, _vp]),
+    "tk_dense_f32": (_i, [_vp, _vp, _vp, _vp, _i, _i, _i, _vp, _vp]),
     "tk_pack_binary": (_i, [_vp, _vp, _sz, _vp, _vp]),
     "tk_binary_dot_batched": (_i, [_vp, _vp, _vp, _sz, _sz, _sz, _vp, _vp]),
     "tk_multibit_dot_batched": (_i, [_vp, _vp, _i, _vp, _i, _vp, _vp, _sz, _sz, _sz, _vp, _vp]),

@@ -56,6 +56,55 @@ __global__ void k_relu(float* __restrict__ z, long long count) {
   }
 }
 
+// Dense fp32 layer for the ResNet head (outside the ternary path; no
+// reference operation order to follow): y[b][o] = bias[o] + sum_k x[b][k] w[o][k]
+// as one fp32 FMA chain in k order.  64 x 64 output tiles, 256 threads with
+// 4 x 4 outputs each, K staged through shared memory 16 at a time.
+__global__ void __launch_bounds__(256) k_dense_f32(const float* __restrict__ x, const float* __restrict__ w,
+                                                   const float* __restrict__ bias, int batch, int in_dim,
+                                                   int out_dim, float* __restrict__ y) {
+  __shared__ float sx[16][64 + 4], sw[16][64 + 4];  // [k][row]
+  const int b0 = blockIdx.y * 64, o0 = blockIdx.x * 64;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;  // outputs (b0 + ty*4 + i, o0 + tx*4 + j)
+  float acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0f;
+  for (int k0 = 0; k0 < in_dim; k0 += 16) {
+    for (int t = threadIdx.x; t < 16 * 64; t += 256) {  // coalesced along k
+      const int r = t >> 4, kk = t & 15, k = k0 + kk;
+      sx[kk][r] = (b0 + r < batch && k < in_dim) ? __ldg(x + (size_t)(b0 + r) * in_dim + k) : 0.0f;
+      sw[kk][r] = (o0 + r < out_dim && k < in_dim) ? __ldg(w + (size_t)(o0 + r) * in_dim + k) : 0.0f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      float xv[4], wv[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        xv[i] = sx[kk][ty * 4 + i];
+        wv[i] = sw[kk][tx * 4 + i];
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = __fmaf_rn(xv[i], wv[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int b = b0 + ty * 4 + i;
+    if (b >= batch) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int o = o0 + tx * 4 + j;
+      if (o < out_dim) y[(size_t)b * out_dim + o] = __fadd_rn(acc[i][j], bias ? __ldg(bias + o) : 0.0f);
+    }
+  }
+}
+
 unsigned grid_of(long long work) {
   const long long g = (work + 255) / 256;
   return (unsigned)(g < 1 ? 1 : (g > 148 * 32 ? 148 * 32 : g));
@@ -74,6 +123,16 @@ int tk_matmul_t(tk_context* ctx, const float* x, const float* w, const float* bi
   cudaStream_t s = (cudaStream_t)stream;
   k_matmul_t<<<grid_of(total), 256, 0, s>>>(x, w, bias, batch, in_dim, out_dim, y);
   if (relu) k_relu<<<grid_of(total), 256, 0, s>>>(y, total);
+  return cudaGetLastError() == cudaSuccess ? TK_OK : TK_ERR_CUDA;
+}
+
+int tk_dense_f32(tk_context* ctx, const float* x, const float* w, const float* bias, int batch, int in_dim,
+                 int out_dim, float* y, void* stream) {
+  TK_ON_DEVICE(ctx);
+  if (!ctx || !x || !w || !y || batch < 0 || in_dim <= 0 || out_dim <= 0) return TK_ERR_INVALID;
+  if (batch == 0) return TK_OK;
+  const dim3 grid((out_dim + 63) / 64, (batch + 63) / 64);
+  k_dense_f32<<<grid, 256, 0, (cudaStream_t)stream>>>(x, w, bias, batch, in_dim, out_dim, y);
   return cudaGetLastError() == cudaSuccess ? TK_OK : TK_ERR_CUDA;
 }
 

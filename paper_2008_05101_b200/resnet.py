@@ -212,7 +212,14 @@ class TernaryResNet:
         return out
 
     def head(self, pooled: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
-        return torch.addmm(self.head_b, pooled, self.head_w.t(), beta=1.0, alpha=1.0, out=out)
+        """fp32 dense head (tk_dense_f32: one FMA chain per logit)."""
+        pooled = pooled.contiguous()
+        if out is None:
+            out = torch.empty((pooled.shape[0], self.head_w.shape[0]), dtype=torch.float32, device="cuda")
+        check(T.lib().tk_dense_f32(tk.context(), pooled.data_ptr(), self.head_w.data_ptr(), self.head_b.data_ptr(),
+                                   pooled.shape[0], pooled.shape[1], self.head_w.shape[0], out.data_ptr(),
+                                   tk._stream()), "tk_dense_f32")
+        return out
 
     def forward(self, images: torch.Tensor, check_errors: bool = False) -> torch.Tensor:
         x = self.stem(images)

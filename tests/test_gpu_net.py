@@ -183,3 +183,19 @@ def test_stem_conv_matches_fp32_reference(tk):
     with torch.backends.cudnn.flags(enabled=True, allow_tf32=False):
         ref = torch.nn.functional.conv2d(x.double(), net.stem_w.double(), stride=2, padding=3)
     assert torch.allclose(y.double(), ref, rtol=1e-5, atol=1e-5)
+
+
+def test_dense_head_matches_fp64(tk):
+    """tk_dense_f32 (the ResNet head, one fp32 FMA chain per logit) vs an fp64
+    matmul, ragged tiles included."""
+    from paper_2008_05101_b200 import _lib as T
+    for (b, k, o) in ((256, 512, 1000), (5, 2048, 70), (64, 17, 64)):
+        x = torch.randn(b, k, device="cuda")
+        w = torch.randn(o, k, device="cuda") / k ** 0.5
+        bias = torch.randn(o, device="cuda")
+        y = torch.empty(b, o, device="cuda")
+        T.check(T.lib().tk_dense_f32(tk.context(), x.data_ptr(), w.data_ptr(), bias.data_ptr(), b, k, o,
+                                     y.data_ptr(), tk._stream()), "dense")
+        ref = x.double() @ w.double().t() + bias.double()
+        scale = x.double().abs() @ w.double().abs().t() + bias.double().abs()
+        assert ((y.double() - ref).abs() / scale).max().item() < k * 1.2e-7
