@@ -784,13 +784,14 @@ __global__ void k_pack_input(const PackIn p) {
     const int y = (int)(pix / p.W), xx = (int)(pix - (long long)y * p.W);
     const float* src = p.x + ((long long)n * p.C + g * 16) * HW + pix;
     float v[16];
-    bool bad = false;
+    float z = 0.0f, mn = 0.0f;  // NaN / inf and negative checks, as in k_pack_input_rows
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
       v[j] = __ldg(src + j * HW);
-      bad |= !(v[j] >= 0.0f && v[j] <= 3.402823466e38f);
+      z = __fmaf_rn(v[j], 0.0f, z);
+      mn = fminf(mn, v[j]);
     }
-    if (bad) {
+    if (z != z || mn < 0.0f) {
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         const int e = tk_error_code(v[j], 1);
@@ -812,12 +813,13 @@ __global__ void k_pack_input(const PackIn p) {
 #pragma unroll
         for (int i2 = 0; i2 < 4; ++i2) {
           const float xv = v[4 * j + i2];
-          b |= ((uint32_t)(xv > p.t0[o]) + (uint32_t)(xv > p.t1[o])) << (8 * i2);
+          if (xv > p.t0[o]) b += 1u << (8 * i2);
+          if (xv > p.t1[o]) b += 1u << (8 * i2);
         }
         w[j] = b;
       }
-      const int Rq = p.q_R[o];
-      const int c0 = g * 16, chq = c0 / Rq, cq = c0 - chq * Rq;
+      const int Rq = p.q_R[o];  // 64 or 128
+      const int c0 = g * 16, chq = Rq == 128 ? c0 >> 7 : c0 >> 6, cq = c0 - chq * Rq;
       const long long off = p.q_phases[o] == 4 ? ((long long)(chq * 4 + ph4) * p.q_pos[o] + P4) * Rq + cq
                                                : ((long long)chq * p.q_pos[o] + P1) * Rq + cq;
       *reinterpret_cast<uint4*>(p.q[o] + off) = make_uint4(w[0], w[1], w[2], w[3]);
@@ -846,13 +848,17 @@ __global__ void __launch_bounds__(256) k_pack_input_rows(const PackIn p) {
     for (int g = 0; g < groups; ++g) {
       const float* src = p.x + ((long long)n * p.C + g * 16) * HW + pix;
       float v[16];
-      bool bad = false;
+      // quantizer input checks (R:quantizer.hpp:37-41,53-55): v * 0 is NaN
+      // exactly for NaN / +-inf, and the minimum is < 0 exactly when some
+      // value is negative (-0.0 is not): two instructions per value
+      float z = 0.0f, mn = 0.0f;
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         v[j] = __ldg(src + (long long)j * HW);
-        bad |= !(v[j] >= 0.0f && v[j] <= 3.402823466e38f);
+        z = __fmaf_rn(v[j], 0.0f, z);
+        mn = fminf(mn, v[j]);
       }
-      if (bad) {
+      if (z != z || mn < 0.0f) {
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
           const int e = tk_error_code(v[j], 1);
@@ -868,14 +874,15 @@ __global__ void __launch_bounds__(256) k_pack_input_rows(const PackIn p) {
         for (int j = 0; j < 4; ++j) {
           uint32_t b = 0;
 #pragma unroll
-          for (int i2 = 0; i2 < 4; ++i2) {
+          for (int i2 = 0; i2 < 4; ++i2) {  // level byte = (x > t0) + (x > t1): predicated adds
             const float xv = v[4 * j + i2];
-            b |= ((uint32_t)(xv > p.t0[o]) + (uint32_t)(xv > p.t1[o])) << (8 * i2);
+            if (xv > p.t0[o]) b += 1u << (8 * i2);
+            if (xv > p.t1[o]) b += 1u << (8 * i2);
           }
           w[j] = b;
         }
-        const int Rq = p.q_R[o];
-        const int c0 = g * 16, chq = c0 / Rq, cq = c0 - chq * Rq;
+        const int Rq = p.q_R[o];  // 64 or 128
+        const int c0 = g * 16, chq = Rq == 128 ? c0 >> 7 : c0 >> 6, cq = c0 - chq * Rq;
         const long long off = p.q_phases[o] == 4 ? ((long long)(chq * 4 + ph4) * p.q_pos[o] + P4) * Rq + cq
                                                  : ((long long)chq * p.q_pos[o] + P1) * Rq + cq;
         *reinterpret_cast<uint4*>(p.q[o] + off) = make_uint4(w[0], w[1], w[2], w[3]);
