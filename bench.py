@@ -832,6 +832,8 @@ def run_ours(args) -> None:
     for k in ("per_layer", "launches_timed", "launch_ms_by_method"):
         if k in r:
             roof[k] = r[k]
+    if r["bound"] == "tensor" and r.get("pipe") == "fp4":  # the same time against the int8 tensor peak
+        roof["frac_of_int8_peak"] = round(achieved / peaks["i8_tc_tops"], 4)
     h2d, d2h = w.e2e_bytes()
     if getattr(w, "world", 1) != world:  # replicated workload: every rank moves its own bytes
         h2d, d2h = h2d * world, d2h * world
