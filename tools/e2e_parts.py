@@ -5,7 +5,7 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
-from paper_2008_05101_b200.resnet import ResNetWorkload  # noqa: E402
+from bench import ResNetWorkload  # noqa: E402
 
 
 def t(fn, n=10):

@@ -12,9 +12,9 @@ from paper_2008_05101_b200.resnet import PipelinedResNet  # noqa: E402
 
 def main():
     w = ResNetWorkload(os.environ.get("W", "resnet18"))
-    if os.environ.get("GROUPS"):  # e.g. GROUPS=5,3 (CHUNKS default 8)
+    if os.environ.get("PIPE_GROUPS"):  # e.g. PIPE_GROUPS=5,3 (bash reserves GROUPS) (CHUNKS default 8)
         w.pipe = PipelinedResNet(w.net, w.B, int(os.environ.get("CHUNKS", 8)),
-                                 [int(g) for g in os.environ["GROUPS"].split(",")])
+                                 [int(g) for g in os.environ["PIPE_GROUPS"].split(",")])
     pipe = w.pipe
     for _ in range(3):
         w.step_e2e()
