@@ -460,7 +460,7 @@ class DotWorkload:
 
     def roofline(self, flush) -> dict:
         ms = _time_graph(graph_of(self.step), flush)
-        return {"kernel": "k_dot_batched (LOP3 + POPC, warp per pair)", "bound": "hbm",
+        return {"kernel": "k_dot_fixed<2> (LOP3 + POPC, warp per pair, compile-time row length)", "bound": "hbm",
                 "work": self.P * self.bytes_per_pair / 1e9, "unit": "GB/s", "avg_launch_ms": ms,
                 "algorithmic": f"{self.bytes_per_pair} B/pair x {self.P} pairs per launch"}
 
