@@ -273,8 +273,10 @@ int tk_net_forward(tk_context* ctx, tk_net* net, const float* x, float* out,
 int tk_affine_relu_maxpool(tk_context* ctx, const float* x, int n, int c, int h, int w,
                            const float* gain, const float* bias, float* out, void* stream);
 /* Network stem helper: 7x7 / stride 2 / pad 3 convolution, 3 -> 64 channels,
- * fp32 FMA in (ci, ky, kx) order: images [n][3][h][w] (w <= 224), weights
- * [64][3][7][7] -> out [n][64][(h-1)/2+1][(w-1)/2+1] (no bias). */
+ * on the tensor cores as split TF32 (x_hi w_hi + x_hi w_lo + x_lo w_hi, f32
+ * accumulation; error <= 4e-6 x sum |x||w| per output): images [n][3][h][w]
+ * (w <= 240), weights [64][3][7][7] -> out [n][64][(h-1)/2+1][(w-1)/2+1]
+ * (no bias); TK_ERR_UNSUPPORTED for wider images. */
 int tk_stem_conv7x7s2(tk_context* ctx, const float* images, int n, int h, int w, const float* weights,
                       float* out, void* stream);
 /* number of kernel launches one tk_net_forward issues */

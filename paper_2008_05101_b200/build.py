@@ -17,7 +17,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libternkit_b200.so")
 PROFILE_OUT = os.path.join(os.path.dirname(HERE), "tools", "libternkit_b200_profile.so")
-SOURCES = ["tk_api.cu", "tk_codec.cu", "tk_popc.cu", "tk_tc.cu", "tk_net.cu", "tk_mlp.cu", "tk_binary.cu"]
+SOURCES = ["tk_api.cu", "tk_codec.cu", "tk_popc.cu", "tk_tc.cu", "tk_net.cu", "tk_mlp.cu", "tk_binary.cu", "tk_stem.cu"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = [

@@ -36,6 +36,10 @@ inline constexpr int tk_knob(const char*, int dflt) { return dflt; }
 // once per (kernel, current device), thread-safe (tk_api.cu).
 cudaError_t tk_smem_attr(const void* kernel, int bytes);
 
+// split-TF32 tensor-core stem conv 7x7/2 (tk_stem.cu)
+int tk_launch_stem_tc(tk_context* ctx, const float* images, int n, int h, int w, const float* weights, float* out,
+                      void* stream);
+
 #define TK_KAUXI32 0x55555555u
 
 struct tk_context {

@@ -1883,8 +1883,9 @@ int tk_stem_conv7x7s2(tk_context* ctx, const float* images, int n, int h, int w,
   TK_ON_DEVICE(ctx);
   if (!ctx || !images || !weights || !out || n < 0 || h <= 0 || w <= 0) return TK_ERR_INVALID;
   const int ho = (h + 6 - 7) / 2 + 1, wo = (w + 6 - 7) / 2 + 1;
-  if (wo > kStemCols || (w + 6) > kStemInCols) return TK_ERR_UNSUPPORTED;  // one CTA spans the width
   if (n == 0) return TK_OK;
+  if (!tk_knob("TK_STEM_SIMT", 0)) return tk_launch_stem_tc(ctx, images, n, h, w, weights, out, stream);
+  if (wo > kStemCols || (w + 6) > kStemInCols) return TK_ERR_UNSUPPORTED;  // one CTA spans the width
   const int smem = (147 * 64 + 2 * 3 * kStemInRows * 2 * kStemPitch) * 4;
   // 8 channels x packed FFMA2 per thread, 512 threads (the fastest of the
   // 8/16-channel, FFMA/FFMA2 variants measured)

@@ -8,7 +8,7 @@ z = max(conv(h) + shortcut, 0).  As in the paper's protocol
 the first (7x7 stem) and last (FC head) layers stay in float.
 
     TernaryBody      -- the ternary hot path (tk_net_* C-ABI, CUDA)
-    TernaryResNet    -- float stem (cuDNN) + TernaryBody + float head
+    TernaryResNet    -- float stem (split-TF32 tensor cores) + TernaryBody + float head
     resnet_spec()    -- synthetic random-weight ResNet-18 / ResNet-50 bodies
 """
 from __future__ import annotations
@@ -194,9 +194,10 @@ class TernaryResNet:
         self.head_b = torch.zeros(classes).cuda()
 
     def stem(self, images: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
-        """fp32 7x7/2 conv (tk_stem_conv7x7s2: SIMT FMA, no tensor-core
-        rounding), then one fused pass of folded BN (fmaf), ReLU and 3x3/2
-        max-pool (tk_affine_relu_maxpool)."""
+        """fp32-class 7x7/2 conv (tk_stem_conv7x7s2: split-TF32 tcgen05,
+        x_hi w_hi + x_hi w_lo + x_lo w_hi, error <= 4e-6 x sum |x||w|), then one
+        fused pass of folded BN (fmaf), ReLU and 3x3/2 max-pool
+        (tk_affine_relu_maxpool)."""
         images = images.contiguous()
         n = images.shape[0]
         y = torch.empty((n, 64, 112, 112), dtype=torch.float32, device="cuda")

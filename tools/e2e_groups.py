@@ -17,8 +17,12 @@ def main():
     net = TernaryResNet(depth, batch, 0)
     imgs = torch.rand(batch, 3, 224, 224, generator=torch.Generator().manual_seed(1)).pin_memory()
     out_host = torch.empty((batch, 1000)).pin_memory()
-    settings = [(8, [3, 5]), (8, [4, 4]), (8, [5, 3]), (8, [6, 2]), (8, [4, 2, 2]), (16, [8, 4, 4]),
-                (16, [10, 6]), (16, [12, 4]), (8, [2, 2, 2, 2]), (4, [3, 1])]
+    settings = [(8, [3, 5]), (8, [4, 4]), (8, [2, 2, 2, 2]), (8, [1] * 8), (8, [2, 2, 2, 1, 1]), (8, [4, 2, 1, 1]),
+                (8, [3, 3, 2]), (16, [4, 4, 4, 4]), (16, [2] * 8), (16, [4, 4, 4, 2, 2]), (16, [1] * 16),
+                (4, [1] * 4)]
+    if os.environ.get("SETTINGS"):  # e.g. "8:3,5;16:4,4,4,4"
+        settings = [(int(c), [int(g) for g in gs.split(",")])
+                    for c, gs in (item.split(":") for item in os.environ["SETTINGS"].split(";"))]
     for chunks, groups in settings:
         pipe = PipelinedResNet(net, batch, chunks, groups)
 
