@@ -58,28 +58,66 @@ __global__ void k_relu(float* __restrict__ z, long long count) {
 
 // Dense fp32 layer for the ResNet head (outside the ternary path; no
 // reference operation order to follow): y[b][o] = bias[o] + sum_k x[b][k] w[o][k]
-// as one fp32 FMA chain in k order.  64 x 64 output tiles, 256 threads with
-// 4 x 4 outputs each, K staged through shared memory 16 at a time.
-__global__ void __launch_bounds__(256) k_dense_f32(const float* __restrict__ x, const float* __restrict__ w,
-                                                   const float* __restrict__ bias, int batch, int in_dim,
-                                                   int out_dim, float* __restrict__ y) {
-  __shared__ float sx[16][64 + 4], sw[16][64 + 4];  // [k][row]
-  const int b0 = blockIdx.y * 64, o0 = blockIdx.x * 64;
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;  // outputs (b0 + ty*4 + i, o0 + tx*4 + j)
+// as one fp32 FMA chain in k order.  32 x 32 output tiles (ResNet head b256:
+// 256 CTAs, not 64), 64 threads with 4 x 4 outputs each, K staged through
+// shared memory 32 at a time; the next K chunk is loaded into registers while
+// the current one is multiplied (the chunk loads are L2/HBM-latency bound).
+constexpr int kDT = 32, kDK = 32;
+__global__ void __launch_bounds__(64) k_dense_f32(const float* __restrict__ x, const float* __restrict__ w,
+                                                  const float* __restrict__ bias, int batch, int in_dim,
+                                                  int out_dim, float* __restrict__ y) {
+  __shared__ float sx[kDK][kDT + 4], sw[kDK][kDT + 4];  // [k][row]
+  const int b0 = blockIdx.y * kDT, o0 = blockIdx.x * kDT;
+  const int tx = threadIdx.x & 7, ty = threadIdx.x >> 3;  // outputs (b0 + ty*4 + i, o0 + tx*4 + j)
+  // loads: 16 rows x 32 k per matrix and pass, thread t -> row (t >> 3) + 8 q, k = 4 (t & 7) .. +3
+  const int lr = threadIdx.x >> 3, lk = (threadIdx.x & 7) * 4;
+  float4 px[4], pw[4];
+  auto load = [&](int k0) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int r = lr + 8 * q, k = k0 + lk;
+      float4 vx = make_float4(0.0f, 0.0f, 0.0f, 0.0f), vw = vx;
+      if (b0 + r < batch) {
+        const float* src = x + (size_t)(b0 + r) * in_dim + k;
+        if (k + 3 < in_dim && ((in_dim & 3) == 0)) vx = __ldg(reinterpret_cast<const float4*>(src));
+        else {
+          vx.x = k < in_dim ? __ldg(src) : 0.0f;
+          vx.y = k + 1 < in_dim ? __ldg(src + 1) : 0.0f;
+          vx.z = k + 2 < in_dim ? __ldg(src + 2) : 0.0f;
+          vx.w = k + 3 < in_dim ? __ldg(src + 3) : 0.0f;
+        }
+      }
+      if (o0 + r < out_dim) {
+        const float* src = w + (size_t)(o0 + r) * in_dim + k;
+        if (k + 3 < in_dim && ((in_dim & 3) == 0)) vw = __ldg(reinterpret_cast<const float4*>(src));
+        else {
+          vw.x = k < in_dim ? __ldg(src) : 0.0f;
+          vw.y = k + 1 < in_dim ? __ldg(src + 1) : 0.0f;
+          vw.z = k + 2 < in_dim ? __ldg(src + 2) : 0.0f;
+          vw.w = k + 3 < in_dim ? __ldg(src + 3) : 0.0f;
+        }
+      }
+      px[q] = vx;
+      pw[q] = vw;
+    }
+  };
   float acc[4][4];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j] = 0.0f;
-  for (int k0 = 0; k0 < in_dim; k0 += 16) {
-    for (int t = threadIdx.x; t < 16 * 64; t += 256) {  // coalesced along k
-      const int r = t >> 4, kk = t & 15, k = k0 + kk;
-      sx[kk][r] = (b0 + r < batch && k < in_dim) ? __ldg(x + (size_t)(b0 + r) * in_dim + k) : 0.0f;
-      sw[kk][r] = (o0 + r < out_dim && k < in_dim) ? __ldg(w + (size_t)(o0 + r) * in_dim + k) : 0.0f;
+  load(0);
+  for (int k0 = 0; k0 < in_dim; k0 += kDK) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int r = lr + 8 * q;
+      sx[lk][r] = px[q].x; sx[lk + 1][r] = px[q].y; sx[lk + 2][r] = px[q].z; sx[lk + 3][r] = px[q].w;
+      sw[lk][r] = pw[q].x; sw[lk + 1][r] = pw[q].y; sw[lk + 2][r] = pw[q].z; sw[lk + 3][r] = pw[q].w;
     }
     __syncthreads();
+    if (k0 + kDK < in_dim) load(k0 + kDK);  // in flight while this chunk is multiplied
 #pragma unroll
-    for (int kk = 0; kk < 16; ++kk) {
+    for (int kk = 0; kk < kDK; ++kk) {
       float xv[4], wv[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
@@ -131,8 +169,8 @@ int tk_dense_f32(tk_context* ctx, const float* x, const float* w, const float* b
   TK_ON_DEVICE(ctx);
   if (!ctx || !x || !w || !y || batch < 0 || in_dim <= 0 || out_dim <= 0) return TK_ERR_INVALID;
   if (batch == 0) return TK_OK;
-  const dim3 grid((out_dim + 63) / 64, (batch + 63) / 64);
-  k_dense_f32<<<grid, 256, 0, (cudaStream_t)stream>>>(x, w, bias, batch, in_dim, out_dim, y);
+  const dim3 grid((out_dim + kDT - 1) / kDT, (batch + kDT - 1) / kDT);
+  k_dense_f32<<<grid, 64, 0, (cudaStream_t)stream>>>(x, w, bias, batch, in_dim, out_dim, y);
   return cudaGetLastError() == cudaSuccess ? TK_OK : TK_ERR_CUDA;
 }
 

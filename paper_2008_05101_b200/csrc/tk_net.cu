@@ -1713,9 +1713,11 @@ cudaError_t launch_conv(const Conv& cv, const float* x, float* out, int pdl, cud
   if (cv.skip_f == -2) k.skip = x;  // identity shortcut = the forward's input
   if (cv.out_f == -3) k.fout = out;  // the caller's output (conv2d_ternary plans)
   // programmatic dependent launch: the prologue (TMEM, barriers, resident
-  // weights) may overlap the previous kernel's tail.  Off inside the network:
-  // with one persistent CTA per SM no SM frees early enough for it to pay
-  // off (measured); on for conv2d_ternary plans, behind the input packing.
+  // weights) may overlap the previous kernel's tail.  Inside the network only
+  // for batches <= 128 (tools/body_batch.py, ResNet-18 body: b32 -11%, b64
+  // -9%, b128 -6%, b256 -1.5%; ResNet-50 b128 -2%, b256 +1.6%, b512 +3.5%):
+  // small layers leave SMs idle in their tails, large ones do not; on for
+  // conv2d_ternary plans, behind the input packing.
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(cv.grid);
   cfg.blockDim = dim3(conv_threads(BN, MT, GPI));
@@ -1994,7 +1996,7 @@ int tk_net_forward(tk_context* ctx, tk_net* net, const float* x, float* out, flo
     for (const auto& cvs : net->convs)
       for (const auto& cv : cvs) {
         if (net->timing) cudaEventRecord(net->ev[2 * ci], s);
-        if (const cudaError_t ce = run_conv(cv, x, nullptr, tk_knob("TK_PDL", 0), s); ce != cudaSuccess) {
+        if (const cudaError_t ce = run_conv(cv, x, nullptr, tk_knob("TK_PDL", net->batch <= 128), s); ce != cudaSuccess) {
           if (tk_knob("TK_NET_DEBUG", 0)) fprintf(stderr, "tk_net_forward: conv %d: %s\n", ci, cudaGetErrorString(ce));
           return TK_ERR_CUDA;
         }

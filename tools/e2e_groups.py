@@ -5,6 +5,9 @@ import os
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+if os.environ.get("PROFILE"):  # the -DTK_PROFILE build (experiment knobs such as TK_PDL)
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    import _profile  # noqa: E402,F401
 import torch  # noqa: E402
 
 import bench  # noqa: E402

@@ -34,4 +34,8 @@ timeout -s KILL 900 ncu --set full --import-source on --clock-control none -k re
 # and of the cfg3 FC GEMM (FP4 pipe, bench tile choice)
 BACKEND=TC_F4 timeout -s KILL 600 ncu --set full --import-source on --clock-control none -k regex:k_gemm_tc -s 2 -c 1 \
   -o gpurun_out/prof/full_fc_gemm python tools/prof_fc.py > gpurun_out/prof/full_fc.log 2>&1
+# and of the split-TF32 stem conv (256 images)
+timeout -s KILL 300 python tools/prof_stem.py > /dev/null 2>&1 &&
+timeout -s KILL 600 ncu --set full --import-source on --clock-control none -k regex:k_stem_tc -s 3 -c 1 \
+  -o gpurun_out/prof/full_stem python tools/prof_stem.py > gpurun_out/prof/full_stem.log 2>&1
 ls -la gpurun_out/prof

@@ -120,7 +120,8 @@ def full(name, rep, note):
                           "dram__bytes_read.sum,dram__bytes_write.sum,lts__t_bytes.sum,"
                           "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active,"
                           "sm__inst_executed_pipe_tc.avg.pct_of_peak_sustained_active,"
-                          "sm__pipe_tc_cycles_active.avg.pct_of_peak_sustained_active"],
+                          "sm__pipe_tc_cycles_active.avg.pct_of_peak_sustained_active,"
+                          "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active"],
                          capture_output=True, text=True).stdout
     with open(os.path.join(OUT, f"ncu_full_r02_{name}.txt"), "w") as f:
         f.write(note + "\n\n")
@@ -152,6 +153,10 @@ def main():
     full("fc_gemm", "full_fc_gemm.ncu-rep",
          "BACKEND=TC_F4 ncu --set full --clock-control none -k regex:k_gemm_tc -s 2 -c 1 python tools/prof_fc.py\n"
          "(cfg3 FC 4096x4096 b256, FP4 pipe, int32 out, tile chosen by the launcher; ncu flushes caches)")
+    full("stem", "full_stem.ncu-rep",
+         "ncu --set full --clock-control none -k regex:k_stem_tc -s 3 -c 1 python tools/prof_stem.py\n"
+         "(ResNet stem 7x7/2 3->64, 256 x 224x224 images, split-TF32 tcgen05 kind::tf32: 84 MMAs 128x64x8 "
+         "per 128-position tile; the kernel is bound by the MMAs' shared-memory operand reads)")
 
 
 if __name__ == "__main__":
