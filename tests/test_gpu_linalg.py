@@ -276,6 +276,8 @@ FUSED_CASES = [  # (c, oc, h, w, k, stride, n)
     (256, 512, 8, 8, 3, 1, 1),
     (64, 64, 9, 10, 3, 1, 2),
     (128, 64, 12, 8, 1, 1, 3),
+    (64, 256, 14, 14, 3, 1, 2),    # one 256-wide N tile over 64-channel rows
+    (64, 64, 56, 56, 3, 1, 16),    # 421 tiles: several items per persistent CTA
 ]
 
 
