@@ -86,7 +86,8 @@ struct ConvK {
   const float* gain;
   const float* bias;
   const int* ithr;  // [n_q][3][N] (c0, c1, sign) integer-threshold mode, or null
-  int ithr16;       // ithr holds [n_q][N] (c0 & 0xffff) | c1 << 16 (all signs +1)
+  int ithr16;       // 1: ithr holds [n_q][N] (c0 & 0xffff) | c1 << 16 (all signs +1);
+                    // 2: per channel pair (-c0, -c0') and (-c1, -c1') as s16x2 (DPX form)
   float out_scale;
   int relu;
   int N;
@@ -522,7 +523,22 @@ k_conv_tc(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
           for (int o = 0; o < 2; ++o) {
             if (o >= p.n_q) break;
             uint32_t w[CH / 4];
-            if (p.ithr16) {
+            if (p.ithr16 == 2) {
+              // channel pairs as s16x2: (acc > c) = max(min(acc - c, 1), 0),
+              // one DPX add-min-relu per threshold and pair; 4 levels -> 4 bytes
+              const uint4* e0 = reinterpret_cast<const uint4*>(ep + o * p.N + n0);
+#pragma unroll
+              for (int j = 0; j < CH / 4; ++j) {
+                const uint4 cc = e0[j];
+                const uint32_t x01 = __byte_perm(r[4 * j], r[4 * j + 1], 0x5410);
+                const uint32_t x23 = __byte_perm(r[4 * j + 2], r[4 * j + 3], 0x5410);
+                const uint32_t l01 = __viaddmin_s16x2_relu(x01, cc.x, 0x00010001u) +
+                                     __viaddmin_s16x2_relu(x01, cc.y, 0x00010001u);
+                const uint32_t l23 = __viaddmin_s16x2_relu(x23, cc.z, 0x00010001u) +
+                                     __viaddmin_s16x2_relu(x23, cc.w, 0x00010001u);
+                w[j] = __byte_perm(l01, l23, 0x6420);
+              }
+            } else if (p.ithr16) {
               // (c0, c1) s16 pairs of 4 channels per 16-byte LDS (broadcast):
               // a third of the shared-memory wavefronts of the general form,
               // which competes with the MMA operand reads
@@ -1660,13 +1676,24 @@ int finish_fused(tk_net* net, int pack_a, int pack_b) {
                      c1 <= 32767;
           }
         if (tk_knob("TK_CONV_NOPACK16", 0)) pack16 = false;
-        k.ithr16 = pack16 ? 1 : 0;
+        // DPX form: level pairs by two s16x2 add-min-relu ops (|acc - c| <= 2 kmax + 1 fits s16)
+        const bool dpx = pack16 && 2 * kmax + 1 <= 32767 && tk_knob("TK_CONV_DPX", 1);
+        k.ithr16 = pack16 ? (dpx ? 2 : 1) : 0;
         if (pack16) {
           std::vector<int> p16((size_t)k.n_q * N);
+          auto h16 = [](int v) { return (uint32_t)v & 0xFFFFu; };
           for (int o = 0; o < k.n_q; ++o)
-            for (int n = 0; n < N; ++n)
-              p16[(size_t)o * N + n] = (int)(((uint32_t)thr[((size_t)o * 3 + 0) * N + n] & 0xFFFFu) |
-                                             ((uint32_t)thr[((size_t)o * 3 + 1) * N + n] << 16));
+            for (int n = 0; n < N; ++n) {
+              const int c0 = thr[((size_t)o * 3 + 0) * N + n], c1 = thr[((size_t)o * 3 + 1) * N + n];
+              if (!dpx) {
+                p16[(size_t)o * N + n] = (int)(h16(c0) | (h16(c1) << 16));
+              } else {  // words of channels 4j..4j+3: (-c0 pair 01, -c1 pair 01, -c0 pair 23, -c1 pair 23)
+                const int j = n & ~3, i = n & 3, word = j + (i >> 1) * 2, hi = i & 1;
+                uint32_t* w = reinterpret_cast<uint32_t*>(p16.data() + (size_t)o * N);
+                w[word] = (w[word] & (hi ? 0xFFFFu : 0xFFFF0000u)) | (h16(-c0) << (16 * hi));
+                w[word + 1] = (w[word + 1] & (hi ? 0xFFFFu : 0xFFFF0000u)) | (h16(-c1) << (16 * hi));
+              }
+            }
           thr.swap(p16);
         }
         if (cudaMalloc(&cv.d_ithr, thr.size() * 4) != cudaSuccess) return TK_ERR_CUDA;
