@@ -63,6 +63,41 @@ def test_fused_path_small_body(oracle):
     _check(oracle, blocks, x, n, c, h, w, expect_fused=True)
 
 
+def _edge_conv(rng, in_c, out_c, k, pad, near, neg_gain):
+    """A conv whose accumulators reach their extremes (weights all +1 or all
+    -1 per row, a few zeros, on level-2 inputs: +-2 nnz at interior positions,
+    kmax = 2 in_c k^2) and whose folded BN puts both quantizer thresholds
+    within a few counts of them (alpha2 - alpha1 = 0.4 = 3 counts)."""
+    K = in_c * k * k
+    sign = rng.choice([1, -1], size=out_c, p=[0.75, 0.25]).astype(np.int8)
+    w = np.repeat(sign[:, None], K, axis=1)
+    w[:, ::97] = 0
+    peak = 2 * np.count_nonzero(w, axis=1).astype(np.float64)  # |acc| at interior positions
+    g = np.full(out_c, 0.4 / 3, np.float64)
+    if neg_gain:
+        g[::5] *= -1
+    ta = (0.5, 0.9)
+    j = np.arange(out_c)
+    acc_t = np.where(sign > 0, peak - near - j % 7, -peak + j % 5)  # alpha1 crossing
+    b = ta[0] - g * (acc_t + 0.5)
+    return dict(in_c=in_c, out_c=out_c, k=k, stride=1, pad=pad, weights=w, ta=ta, tw=(1.0, 1.0),
+                gain=g.astype(np.float32), bias=b.astype(np.float32), out_scale=1.0)
+
+
+@pytest.mark.parametrize("neg_gain", [False, True])
+def test_fused_extreme_accumulators(oracle, neg_gain):
+    """Inner-conv integer thresholds at the accumulator extremes: 512-channel
+    1x1 and 3x3 convs (kmax 1024 / 9216) on level-2 inputs with weights mostly
+    +1 or -1, thresholds within a few counts of +-kmax -- the s16x2 DPX form
+    (all gains positive) and the general signed form (some negative)."""
+    rng = np.random.default_rng(11 + neg_gain)
+    c, n, h, w = 512, 2, 6, 6
+    blocks = [dict(convs=[_edge_conv(rng, c, c, 1, 0, 2, neg_gain), _edge_conv(rng, c, c, 3, 1, 2, neg_gain),
+                          conv_spec(rng, c, c, 1, 1, 0)])]
+    x = (2.0 + rng.random(n * c * h * w)).astype(np.float32)  # every level 2
+    body, out = _check(oracle, blocks, x, n, c, h, w, expect_fused=True)
+
+
 def test_fused_equals_generic(oracle):
     from paper_2008_05101_b200 import _lib as T
     blocks, (n, c, h, w), x = fused_small(seed=5, n=2, h=12, w=20)
