@@ -917,6 +917,9 @@ __global__ void k_residual_relu(float* __restrict__ z, const float* __restrict__
 
 // spatial mean -> [N][C] (head input; left-to-right float sum)
 // ---------------------------------------------------------------------------
+#ifdef TK_PROFILE
+// (profiling build only: the fp32 SIMT stem the split-TF32 tensor-core kernel
+// of tk_stem.cu replaced, kept for the A/B in tools/stem_ab.py)
 // stem convolution (float, outside the ternary path): 7x7 / stride 2 / pad 3,
 // 3 -> 64 channels, fp32 FMA accumulation in the fixed order (ci, ky, kx).
 // CTA = one image, kStemRows output rows x the full width; 512 threads =
@@ -1040,6 +1043,7 @@ k_stem_conv(const float* __restrict__ img, const float* __restrict__ wgt, int N,
     __syncthreads();  // everyone is done with this band before it is refilled
   }
 }
+#endif  // TK_PROFILE
 
 // stem: out = maxpool3x3/2 pad 1 (relu(fmaf(g, x, b))); thread per output
 __global__ void k_affine_relu_maxpool(const float* __restrict__ x, int C, int H, int W, int Ho, int Wo,
@@ -1911,18 +1915,21 @@ int tk_stem_conv7x7s2(tk_context* ctx, const float* images, int n, int h, int w,
                       float* out, void* stream) {
   TK_ON_DEVICE(ctx);
   if (!ctx || !images || !weights || !out || n < 0 || h <= 0 || w <= 0) return TK_ERR_INVALID;
-  const int ho = (h + 6 - 7) / 2 + 1, wo = (w + 6 - 7) / 2 + 1;
   if (n == 0) return TK_OK;
-  if (!tk_knob("TK_STEM_SIMT", 0)) return tk_launch_stem_tc(ctx, images, n, h, w, weights, out, stream);
-  if (wo > kStemCols || (w + 6) > kStemInCols) return TK_ERR_UNSUPPORTED;  // one CTA spans the width
-  const int smem = (147 * 64 + 2 * 3 * kStemInRows * 2 * kStemPitch) * 4;
-  // 8 channels x packed FFMA2 per thread, 512 threads (the fastest of the
-  // 8/16-channel, FFMA/FFMA2 variants measured)
-  if (tk_smem_attr((const void*)k_stem_conv<8, true>, smem) != cudaSuccess) return TK_ERR_CUDA;
-  const int items = n * ((ho + kStemRows - 1) / kStemRows);
-  k_stem_conv<8, true><<<std::min(items, ctx->num_sms), 512, smem, (cudaStream_t)stream>>>(images, weights, n, h, w,
-                                                                                        ho, wo, out);
-  return cudaGetLastError() == cudaSuccess ? TK_OK : TK_ERR_CUDA;
+#ifdef TK_PROFILE
+  // the fp32 SIMT kernel the tensor-core stem replaced, for A/B (tools/stem_ab.py)
+  if (tk_knob("TK_STEM_SIMT", 0)) {
+    const int ho = (h + 6 - 7) / 2 + 1, wo = (w + 6 - 7) / 2 + 1;
+    if (wo > kStemCols || (w + 6) > kStemInCols) return TK_ERR_UNSUPPORTED;  // one CTA spans the width
+    const int smem = (147 * 64 + 2 * 3 * kStemInRows * 2 * kStemPitch) * 4;
+    if (tk_smem_attr((const void*)k_stem_conv<8, true>, smem) != cudaSuccess) return TK_ERR_CUDA;
+    const int items = n * ((ho + kStemRows - 1) / kStemRows);
+    k_stem_conv<8, true><<<std::min(items, ctx->num_sms), 512, smem, (cudaStream_t)stream>>>(images, weights, n, h,
+                                                                                          w, ho, wo, out);
+    return cudaGetLastError() == cudaSuccess ? TK_OK : TK_ERR_CUDA;
+  }
+#endif
+  return tk_launch_stem_tc(ctx, images, n, h, w, weights, out, stream);
 }
 
 int tk_net_destroy(tk_net* net) {
