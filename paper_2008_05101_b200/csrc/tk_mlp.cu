@@ -58,47 +58,48 @@ __global__ void k_relu(float* __restrict__ z, long long count) {
 
 // Dense fp32 layer for the ResNet head (outside the ternary path; no
 // reference operation order to follow): y[b][o] = bias[o] + sum_k x[b][k] w[o][k]
-// as one fp32 FMA chain in k order.  32 x 32 output tiles (ResNet head b256:
-// 256 CTAs, not 64), 64 threads with 4 x 4 outputs each, K staged through
-// shared memory 32 at a time; the next K chunk is loaded into registers while
-// the current one is multiplied (the chunk loads are L2/HBM-latency bound).
-constexpr int kDT = 32, kDK = 32;
-__global__ void __launch_bounds__(64) k_dense_f32(const float* __restrict__ x, const float* __restrict__ w,
-                                                  const float* __restrict__ bias, int batch, int in_dim,
-                                                  int out_dim, float* __restrict__ y) {
-  __shared__ float sx[kDK][kDT + 4], sw[kDK][kDT + 4];  // [k][row]
+// in fp32.  32 x 32 output tiles (ResNet head b256: 256 CTAs); the K range
+// is split over 4 groups of 64 threads (4 x 4 outputs per thread, one fp32
+// FMA chain per K quarter), each streaming its quarter through a 3-stage
+// cp.async ring of 32-wide chunks; the four partial sums are added in group
+// order at the end (deterministic).  One warp per scheduler was latency
+// bound (81 / 29 us for the b256 head); 8 warps per CTA hide it.
+constexpr int kDT = 32, kDK = 32, kDS = 3, kDG = 4;
+struct DenseSmem {
+  float x[kDG][kDS][kDT][kDK + 4];  // [group][stage][row][k]
+  float w[kDG][kDS][kDT][kDK + 4];
+};
+__global__ void __launch_bounds__(64 * kDG) k_dense_f32(const float* __restrict__ x, const float* __restrict__ w,
+                                                        const float* __restrict__ bias, int batch, int in_dim,
+                                                        int out_dim, float* __restrict__ y) {
+  extern __shared__ __align__(16) uint8_t dense_raw[];
+  DenseSmem& sm = *reinterpret_cast<DenseSmem*>(dense_raw);
+  const int g = threadIdx.x >> 6, t = threadIdx.x & 63;
   const int b0 = blockIdx.y * kDT, o0 = blockIdx.x * kDT;
-  const int tx = threadIdx.x & 7, ty = threadIdx.x >> 3;  // outputs (b0 + ty*4 + i, o0 + tx*4 + j)
-  // loads: 16 rows x 32 k per matrix and pass, thread t -> row (t >> 3) + 8 q, k = 4 (t & 7) .. +3
-  const int lr = threadIdx.x >> 3, lk = (threadIdx.x & 7) * 4;
-  float4 px[4], pw[4];
-  auto load = [&](int k0) {
+  const int tx = t & 7, ty = t >> 3;  // outputs (b0 + ty + 8 i, o0 + tx + 8 j)
+  const bool vec = (in_dim & 3) == 0;
+  const int nch_all = (in_dim + kDK - 1) / kDK, per = (nch_all + kDG - 1) / kDG;
+  const int c_begin = g * per, nch = max(0, min(nch_all, c_begin + per) - c_begin);
+  const int nmax = per;  // chunk count of the largest group (uniform trip count for the barriers)
+  auto stage = [&](int c) {  // chunk c of this group: rows t / 8 + 8 q, k = 4 (t % 8) .. +3
+    const int st = c % kDS, k0 = (c_begin + c) * kDK, lk = (t & 7) * 4;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const int r = lr + 8 * q, k = k0 + lk;
-      float4 vx = make_float4(0.0f, 0.0f, 0.0f, 0.0f), vw = vx;
-      if (b0 + r < batch) {
-        const float* src = x + (size_t)(b0 + r) * in_dim + k;
-        if (k + 3 < in_dim && ((in_dim & 3) == 0)) vx = __ldg(reinterpret_cast<const float4*>(src));
-        else {
-          vx.x = k < in_dim ? __ldg(src) : 0.0f;
-          vx.y = k + 1 < in_dim ? __ldg(src + 1) : 0.0f;
-          vx.z = k + 2 < in_dim ? __ldg(src + 2) : 0.0f;
-          vx.w = k + 3 < in_dim ? __ldg(src + 3) : 0.0f;
+      const int r = (t >> 3) + 8 * q, k = k0 + lk;
+#pragma unroll
+      for (int m = 0; m < 2; ++m) {
+        const int row = (m ? o0 : b0) + r, rows = m ? out_dim : batch;
+        const float* src = (m ? w : x) + (size_t)row * in_dim + k;
+        float* dst = m ? &sm.w[g][st][r][lk] : &sm.x[g][st][r][lk];
+        if (vec && row < rows && k + 3 < in_dim) {
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+                       "l"(src)
+                       : "memory");
+        } else {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) dst[e] = (row < rows && k + e < in_dim) ? __ldg(src + e) : 0.0f;
         }
       }
-      if (o0 + r < out_dim) {
-        const float* src = w + (size_t)(o0 + r) * in_dim + k;
-        if (k + 3 < in_dim && ((in_dim & 3) == 0)) vw = __ldg(reinterpret_cast<const float4*>(src));
-        else {
-          vw.x = k < in_dim ? __ldg(src) : 0.0f;
-          vw.y = k + 1 < in_dim ? __ldg(src + 1) : 0.0f;
-          vw.z = k + 2 < in_dim ? __ldg(src + 2) : 0.0f;
-          vw.w = k + 3 < in_dim ? __ldg(src + 3) : 0.0f;
-        }
-      }
-      px[q] = vx;
-      pw[q] = vw;
     }
   };
   float acc[4][4];
@@ -106,39 +107,62 @@ __global__ void __launch_bounds__(64) k_dense_f32(const float* __restrict__ x, c
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j] = 0.0f;
-  load(0);
-  for (int k0 = 0; k0 < in_dim; k0 += kDK) {
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int r = lr + 8 * q;
-      sx[lk][r] = px[q].x; sx[lk + 1][r] = px[q].y; sx[lk + 2][r] = px[q].z; sx[lk + 3][r] = px[q].w;
-      sw[lk][r] = pw[q].x; sw[lk + 1][r] = pw[q].y; sw[lk + 2][r] = pw[q].z; sw[lk + 3][r] = pw[q].w;
-    }
-    __syncthreads();
-    if (k0 + kDK < in_dim) load(k0 + kDK);  // in flight while this chunk is multiplied
-#pragma unroll
-    for (int kk = 0; kk < kDK; ++kk) {
-      float xv[4], wv[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        xv[i] = sx[kk][ty * 4 + i];
-        wv[i] = sw[kk][tx * 4 + i];
-      }
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = __fmaf_rn(xv[i], wv[j], acc[i][j]);
-    }
-    __syncthreads();
+  for (int c = 0; c < kDS - 1; ++c) {
+    if (c < nch) stage(c);
+    asm volatile("cp.async.commit_group;" ::: "memory");
   }
+  for (int c = 0; c < nmax; ++c) {
+    asm volatile("cp.async.wait_group %0;" ::"n"(kDS - 2) : "memory");
+    __syncthreads();  // chunk c landed; chunk c - 1's slot is free
+    if (c + kDS - 1 < nch) stage(c + kDS - 1);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    if (c < nch) {
+      const int st = c % kDS;
+      // 4 k at a time as float4 rows; a thread's rows are 8 apart, so the 8
+      // (4) distinct rows a warp reads sit in distinct 16-byte bank groups
+#pragma unroll
+      for (int kk = 0; kk < kDK; kk += 4) {
+        float4 xq[4], wq[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          xq[i] = *reinterpret_cast<const float4*>(&sm.x[g][st][ty + 8 * i][kk]);
+          wq[i] = *reinterpret_cast<const float4*>(&sm.w[g][st][tx + 8 * i][kk]);
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const float xv = e == 0 ? xq[i].x : e == 1 ? xq[i].y : e == 2 ? xq[i].z : xq[i].w;
+              const float wv = e == 0 ? wq[j].x : e == 1 ? wq[j].y : e == 2 ? wq[j].z : wq[j].w;
+              acc[i][j] = __fmaf_rn(xv, wv, acc[i][j]);
+            }
+      }
+    }
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  __syncthreads();
+  // partial sums of groups 1..3 through shared memory (the x slots), added in group order by group 0
+  float* part = &sm.x[0][0][0][0];
+  if (g > 0) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) part[((g - 1) * 16 + i * 4 + j) * 64 + t] = acc[i][j];
+  }
+  __syncthreads();
+  if (g > 0) return;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    const int b = b0 + ty * 4 + i;
-    if (b >= batch) continue;
+    const int b = b0 + ty + 8 * i;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const int o = o0 + tx * 4 + j;
-      if (o < out_dim) y[(size_t)b * out_dim + o] = __fadd_rn(acc[i][j], bias ? __ldg(bias + o) : 0.0f);
+      float v = acc[i][j];
+#pragma unroll
+      for (int h = 0; h < kDG - 1; ++h) v = __fadd_rn(v, part[(h * 16 + i * 4 + j) * 64 + t]);
+      const int o = o0 + tx + 8 * j;
+      if (b < batch && o < out_dim) y[(size_t)b * out_dim + o] = __fadd_rn(v, bias ? __ldg(bias + o) : 0.0f);
     }
   }
 }
@@ -170,7 +194,8 @@ int tk_dense_f32(tk_context* ctx, const float* x, const float* w, const float* b
   if (!ctx || !x || !w || !y || batch < 0 || in_dim <= 0 || out_dim <= 0) return TK_ERR_INVALID;
   if (batch == 0) return TK_OK;
   const dim3 grid((out_dim + kDT - 1) / kDT, (batch + kDT - 1) / kDT);
-  k_dense_f32<<<grid, 64, 0, (cudaStream_t)stream>>>(x, w, bias, batch, in_dim, out_dim, y);
+  if (tk_smem_attr((const void*)k_dense_f32, (int)sizeof(DenseSmem)) != cudaSuccess) return TK_ERR_CUDA;
+  k_dense_f32<<<grid, 64 * kDG, sizeof(DenseSmem), (cudaStream_t)stream>>>(x, w, bias, batch, in_dim, out_dim, y);
   return cudaGetLastError() == cudaSuccess ? TK_OK : TK_ERR_CUDA;
 }
 

@@ -213,7 +213,7 @@ class TernaryResNet:
         return out
 
     def head(self, pooled: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
-        """fp32 dense head (tk_dense_f32: one FMA chain per logit)."""
+        """fp32 dense head (tk_dense_f32: four K-quarter FMA chains per logit, summed in order)."""
         pooled = pooled.contiguous()
         if out is None:
             out = torch.empty((pooled.shape[0], self.head_w.shape[0]), dtype=torch.float32, device="cuda")
