@@ -230,26 +230,34 @@ class TernaryResNet:
 
 class PipelinedResNet:
     """End-to-end inference from host images.  The batch is uploaded in
-    `chunks` slices on a copy stream; each slice's stem runs (compute stream)
-    as soon as it has landed, and the ternary body runs on groups of
-    consecutive slices (`groups`: slices per body launch sequence, default
-    one group per slice) once their stems are done -- so the body of an
-    early group overlaps the upload of later slices, and only the last
-    group's stem + body follow the final copy.  Shares the stem/head
-    parameters and block spec of `net`."""
+    slices on a copy stream (`chunks` equal slices, or the image counts in
+    `slices`); each slice's stem runs (compute stream) as soon as it has
+    landed, and the ternary body runs on groups of consecutive slices
+    (`groups`: slices per body launch sequence, default one group per slice)
+    once their stems are done -- so the body of an early group overlaps the
+    upload of later slices, and only the last group's stem + body follow the
+    final copy.  Shares the stem/head parameters and block spec of `net`."""
 
-    def __init__(self, net: TernaryResNet, batch: int, chunks: int = 4, groups: list[int] | None = None):
-        assert batch % chunks == 0
+    def __init__(self, net: TernaryResNet, batch: int, chunks: int = 4, groups: list[int] | None = None,
+                 slices: list[int] | None = None):
+        if slices is None:
+            assert batch % chunks == 0
+            slices = [batch // chunks] * chunks
+        slices = list(slices)
+        assert sum(slices) == batch and all(c > 0 for c in slices)
+        chunks = len(slices)
         groups = list(groups) if groups else [1] * chunks
         assert sum(groups) == chunks and all(g > 0 for g in groups)
-        self.net, self.batch, self.chunks, self.cb, self.groups = net, batch, chunks, batch // chunks, groups
-        sizes = sorted(set(groups))
-        self.bodies = {g: TernaryBody(net.blocks, g * self.cb, 64, 56, 56) for g in sizes}
-        self.body = self.bodies[sizes[-1]]
+        self.net, self.batch, self.chunks, self.groups, self.slices = net, batch, chunks, groups, slices
+        self.off = [sum(slices[:i]) for i in range(chunks + 1)]  # image offset of slice i
+        first = [sum(groups[:gi]) for gi in range(len(groups))]   # first slice of group gi
+        self.gsize = [self.off[f + g] - self.off[f] for f, g in zip(first, groups)]  # images per group
+        self.bodies = {n: TernaryBody(net.blocks, n, 64, 56, 56) for n in sorted(set(self.gsize))}
+        self.body = self.bodies[max(self.gsize)]
         self.copy_stream = torch.cuda.Stream()
-        self.img = [torch.empty((self.cb, 3, 224, 224), device="cuda") for _ in range(chunks)]
+        self.img = [torch.empty((c, 3, 224, 224), device="cuda") for c in slices]
         # stem outputs of a group, contiguous so the group's body reads one tensor
-        self.xg = [torch.empty((g * self.cb, 64, 56, 56), device="cuda") for g in groups]
+        self.xg = [torch.empty((n, 64, 56, 56), device="cuda") for n in self.gsize]
         self.ev_copied = [torch.cuda.Event() for _ in range(chunks)]
         self.ev_consumed = [torch.cuda.Event() for _ in range(chunks)]
         self.pooled = torch.empty((batch, self.body.out_shape[0]), device="cuda")
@@ -263,16 +271,17 @@ class PipelinedResNet:
             for i in range(self.chunks):
                 if not self._first:  # the previous step's stem has read this buffer
                     self.copy_stream.wait_event(self.ev_consumed[i])
-                self.img[i].copy_(images_host[i * self.cb:(i + 1) * self.cb], non_blocking=True)
+                self.img[i].copy_(images_host[self.off[i]:self.off[i + 1]], non_blocking=True)
                 self.ev_copied[i].record(self.copy_stream)
         i = 0
         for gi, g in enumerate(self.groups):
-            for k in range(g):
+            g0 = self.off[i]
+            for _ in range(g):
                 cs.wait_event(self.ev_copied[i])
-                self.net.stem(self.img[i], out=self.xg[gi][k * self.cb:(k + 1) * self.cb])
+                self.net.stem(self.img[i], out=self.xg[gi][self.off[i] - g0:self.off[i + 1] - g0])
                 self.ev_consumed[i].record(cs)
                 i += 1
-            lo = (i - g) * self.cb
-            self.bodies[g].forward(self.xg[gi], pooled=self.pooled[lo:lo + g * self.cb], check_errors=False)
+            n = self.gsize[gi]
+            self.bodies[n].forward(self.xg[gi], pooled=self.pooled[g0:g0 + n], check_errors=False)
         self._first = False
         return self.net.head(self.pooled, out=self.logits)

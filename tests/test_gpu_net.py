@@ -199,6 +199,11 @@ def test_pipelined_e2e_matches_serial_chunks(tk):
     got_g = pipe_g.forward(imgs).clone()
     torch.cuda.synchronize()
     assert torch.equal(pipe_g.pooled, pooled) and torch.equal(got_g, got)
+    # uneven slices (4 + 8 + 4 images), bodies on 12 + 4 images: the same bits
+    pipe_u = PipelinedResNet(net, 16, groups=[2, 1], slices=[4, 8, 4])
+    got_u = pipe_u.forward(imgs).clone()
+    torch.cuda.synchronize()
+    assert torch.equal(pipe_u.pooled, pooled) and torch.equal(got_u, got)
     # stem (split-TF32 conv, fused affine + ReLU + max-pool) vs fp64: within
     # the conv's stated bound (4e-6 x sum |x||w|, here <= ~8) x max |gain|
     x = imgs[:2].cuda().double()

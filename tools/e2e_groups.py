@@ -23,11 +23,16 @@ def main():
     settings = [(8, [3, 5]), (8, [4, 4]), (8, [2, 2, 2, 2]), (8, [1] * 8), (8, [2, 2, 2, 1, 1]), (8, [4, 2, 1, 1]),
                 (8, [3, 3, 2]), (16, [4, 4, 4, 4]), (16, [2] * 8), (16, [4, 4, 4, 2, 2]), (16, [1] * 16),
                 (4, [1] * 4)]
-    if os.environ.get("SETTINGS"):  # e.g. "8:3,5;16:4,4,4,4"
-        settings = [(int(c), [int(g) for g in gs.split(",")])
-                    for c, gs in (item.split(":") for item in os.environ["SETTINGS"].split(";"))]
+    if os.environ.get("SETTINGS"):  # e.g. "8:3,5;16:4,4,4,4" or with uneven slices "32,32,48,16:1,1,2"
+        settings = []
+        for item in os.environ["SETTINGS"].split(";"):
+            c, gs = item.split(":")
+            settings.append(([int(v) for v in c.split(",")] if "," in c else int(c), [int(g) for g in gs.split(",")]))
     for chunks, groups in settings:
-        pipe = PipelinedResNet(net, batch, chunks, groups)
+        if isinstance(chunks, list):
+            pipe = PipelinedResNet(net, batch, len(chunks), groups, slices=chunks)
+        else:
+            pipe = PipelinedResNet(net, batch, chunks, groups)
 
         def step():
             y = pipe.forward(imgs)
@@ -36,7 +41,7 @@ def main():
             step()
         torch.cuda.synchronize()
         ms, _, _ = bench.flushed_loop_ms(lambda: [step() for _ in range(10)], lambda: None)
-        print(f"chunks {chunks:2d} groups {str(groups):14s} {ms / 10:.3f} ms/step  {batch / (ms / 10) * 1e3:,.0f} img/s")
+        print(f"chunks {str(chunks):>12s} groups {str(groups):14s} {ms / 10:.3f} ms/step  {batch / (ms / 10) * 1e3:,.0f} img/s")
         del pipe
         torch.cuda.synchronize()
 

@@ -29,7 +29,7 @@ print("body  ms", t(lambda: net.body.forward(w.x, pooled=w.pooled, check_errors=
 print("head  ms", t(lambda: torch.addmm(net.head_b, w.pooled, net.head_w.t())))
 print("e2e   ms", t(w.step_e2e))
 pipe = w.pipe
-cb = pipe.cb
+cb = pipe.slices[0]
 img = torch.empty((cb, 3, 224, 224), device="cuda")
 print(f"chunk of {cb}: h2d ms", t(lambda: img.copy_(w.images_host[:cb], non_blocking=True)),
-      "stem+body ms", t(lambda: pipe.body.forward(net.stem(img), pooled=pipe.pooled[:cb], check_errors=False)))
+      "stem+body ms", t(lambda: pipe.bodies[min(pipe.bodies)].forward(net.stem(img), pooled=pipe.pooled[:cb], check_errors=False)))
