@@ -459,7 +459,10 @@ class DotWorkload:
                 "note": "L2 flushed before each; ops = 2*N*pairs for all three"}
 
     def roofline(self, flush) -> dict:
-        ms = _time_graph(graph_of(self.step), flush)
+        # the operands (134 MB) exceed L2, so launches run back to back as in
+        # the step timing: 10 launches per graph replay (one replay per launch
+        # would add the graph-launch gap, ~1.7 us, to every kernel)
+        ms = _time_graph(graph_of(lambda: [self.step() for _ in range(10)]), flush) / 10
         return {"kernel": "k_dot_fixed<2> (LOP3 + POPC, warp per pair, compile-time row length)", "bound": "hbm",
                 "work": self.P * self.bytes_per_pair / 1e9, "unit": "GB/s", "avg_launch_ms": ms,
                 "algorithmic": f"{self.bytes_per_pair} B/pair x {self.P} pairs per launch"}
