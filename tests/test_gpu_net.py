@@ -232,6 +232,13 @@ def test_stem_conv_matches_fp32_reference(tk):
         ref = torch.nn.functional.conv2d(x.double(), net.stem_w.double(), stride=2, padding=3)
         scale = torch.nn.functional.conv2d(x.double().abs(), net.stem_w.double().abs(), stride=2, padding=3)
         assert ((y.double() - ref).abs() <= 4e-6 * scale + 1e-30).all(), (n, h, w)
+    # wider than one band of the kernel: refused, not silently wrong; n = 0 is a no-op
+    x = torch.rand(1, 3, 8, 256, device="cuda")
+    y = torch.empty(1, 64, 4, 128, device="cuda")
+    assert T.lib().tk_stem_conv7x7s2(tk.context(), x.data_ptr(), 1, 8, 256, net.stem_w.data_ptr(), y.data_ptr(),
+                                     tk._stream()) == T.TK_ERR_UNSUPPORTED
+    assert T.lib().tk_stem_conv7x7s2(tk.context(), x.data_ptr(), 0, 8, 240, net.stem_w.data_ptr(), y.data_ptr(),
+                                     tk._stream()) == T.TK_OK
 
 
 def test_dense_head_matches_fp64(tk):
