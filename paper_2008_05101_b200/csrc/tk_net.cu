@@ -1591,6 +1591,12 @@ int finish_fused(tk_net* net, int pack_a, int pack_b) {
       // (env TK_CONV_HS caps it for experiments)
       const int hs_cap = std::max(1, tk_knob("TK_CONV_HS", 8));
       k.hs = std::max(1, std::min(hs_cap, (budget - wmin) / halo_stage));
+      // streamed 3x3 weights (9 blocks per halo stage) are the bytes that
+      // bound the late stages: the TMA latency times the ring depth caps the
+      // stream, so keep >= 5 weight stages and only 2 halo stages there
+      // (tools/layer_ab.py, ResNet-18 b256: stage-3/4 convs -4..-8%)
+      if (!k.resident && k.n_taps == 9 && tk_knob("TK_CONV_WDEEP", 1))
+        k.hs = std::max(1, std::min(k.hs, std::max(2, (budget - 5 * k.WB) / halo_stage)));
       k.ws = k.resident ? 1 : std::max(2, std::min(8, (budget - k.hs * halo_stage) / k.WB));
       const int wregion = k.resident ? wbytes_all : k.ws * k.WB;
       // epilogue parameter words: at most 2 quantized outputs x 3 ints per channel
