@@ -91,6 +91,37 @@ def body_macs(blocks, h=56, w=56) -> int:
     return macs
 
 
+def body_bytes(blocks, batch: int, in_c: int = 64, h: int = 56, w: int = 56) -> int:
+    """Algorithmic HBM bytes of one fused body forward (the roofline's HBM
+    view): every conv reads its s8 level input once (1 B / element) and its
+    weights once; inner convs write the next conv's levels (1 B); a block's
+    last conv reads the skip (f32 identity, 4 B; s16 downsample
+    accumulators, 2 B) and writes the f32 block output (4 B) plus the next
+    block's levels (1 B, none after the last block); a downsample conv writes
+    its s16 accumulators (2 B).  Halo re-reads, padding rows and duplicate
+    quantizer outputs are not counted."""
+    total = 0
+    c, hh, ww = in_c, h, w
+    for bi, blk in enumerate(blocks):
+        last_blk = bi == len(blocks) - 1
+        h_in, w_in, c_in = hh, ww, c
+        for ci, cv in enumerate(blk["convs"]):
+            ho = (hh + 2 * cv["pad"] - cv["k"]) // cv["stride"] + 1
+            wo = (ww + 2 * cv["pad"] - cv["k"]) // cv["stride"] + 1
+            total += batch * cv["in_c"] * hh * ww + cv["out_c"] * cv["in_c"] * cv["k"] ** 2
+            out = batch * cv["out_c"] * ho * wo
+            if ci < len(blk["convs"]) - 1:
+                total += out
+            else:
+                total += out * (2 if blk.get("down") is not None else 4)  # skip read
+                total += out * 4 + (0 if last_blk else out)
+            hh, ww, c = ho, wo, cv["out_c"]
+        if blk.get("down") is not None:
+            d = blk["down"]
+            total += batch * d["in_c"] * h_in * w_in + d["out_c"] * d["in_c"] + batch * d["out_c"] * hh * ww * 2
+    return total
+
+
 # ---------------------------------------------------------------------------
 # the ternary body on the GPU
 
