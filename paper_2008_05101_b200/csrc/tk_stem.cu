@@ -40,8 +40,8 @@ constexpr int kWBlk = 2 * kCout * 16;  // one tap-pair block: [K chunk][64 rows]
 constexpr int kStages = 8, kAcc = 4;  // stage slot g belongs to producer warp g
 constexpr int kProd = 8, kEpi = 4;  // producer / epilogue warps
 constexpr int kMmaWarp = kProd, kThreads = (kProd + 1 + kEpi) * 32;
-constexpr int kMaxW = 240;
-constexpr uint32_t kDescHi = (128u >> 4) | (1u << 14);  // SBO 128 B, descriptor version 1 (bit 46)  // shared memory: weights 112 KB + 8 stage slots
+constexpr int kMaxW = 240;  // shared memory: weights 112 KB + 8 stage slots
+constexpr uint32_t kDescHi = (128u >> 4) | (1u << 14);  // SBO 128 B, descriptor version 1 (bit 46)
 constexpr int kGroupWarps = 1;  // producer warps per (phase plane, tile parity)
 constexpr int kPer = 17;  // band positions per producer thread per stage (band <= 17 x 32 for W <= 240)
 
