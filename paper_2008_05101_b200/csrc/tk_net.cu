@@ -1551,8 +1551,14 @@ int finish_fused(tk_net* net, int pack_a, int pack_b) {
       // single tile)
       // (measured, tools/layer_ab.py: also pays off for 128-channel stride-2
       // inner convs, not for 128-channel stride-1 ones)
-      const bool wide_mt2 = inner && (cv.d.out_c >= 256 || (cv.d.out_c >= 128 && cv.d.stride == 2)) &&
-                            tk_knob("TK_CONV_WIDE_MT2", 1);
+      // (re-measured after the weight-ring change: the 3x3 stride-1 ones are
+      // faster as 256-wide single tiles again -- ResNet-18 body -1.2%,
+      // ResNet-50 b1024 -0.2%; bits: 1 all stride-1 wide, 4 stride-1 1x1
+      // only, 2 stride-2)
+      const int wm = tk_knob("TK_CONV_WIDE_MT2", 6);
+      const bool wide_mt2 = inner && ((wm & 1) && cv.d.out_c >= 256 && cv.d.stride == 1 ||
+                                      (wm & 4) && cv.d.out_c >= 256 && cv.d.stride == 1 && cv.d.k == 1 ||
+                                      (wm & 2) && cv.d.out_c >= 128 && cv.d.stride == 2);
       int st = prepare_conv_weights(cv, in.R, wide_mt2 ? 128 : 0);
       if (st != TK_OK) return st;
       plan_taps(cv, in);
