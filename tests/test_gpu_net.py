@@ -98,6 +98,45 @@ def test_fused_extreme_accumulators(oracle, neg_gain):
     body, out = _check(oracle, blocks, x, n, c, h, w, expect_fused=True)
 
 
+def _random_body(seed):
+    """A random residual body the fused path accepts: basic or bottleneck
+    blocks, 64/128/256/512 channels, stride-1/2 transitions with downsample,
+    per-conv quantizer thresholds and BN drawn at random."""
+    rng = np.random.default_rng(seed)
+    c, h = 64, int(rng.choice([16, 24, 32]))
+    blocks = []
+    for _ in range(int(rng.integers(3, 6))):
+        out = (2 * c if rng.random() < 0.6 else c) if c < 512 else c
+        stride = 2 if out != c and h % 2 == 0 and h >= 8 else 1
+        if stride == 1 and out != c:
+            out = c
+        ta = lambda: tuple(sorted(rng.uniform(0.3, 1.1, 2)))  # noqa: E731
+        if rng.random() < 0.5:  # basic block
+            convs = [conv_spec(rng, c, out, 3, stride, 1, ta()), conv_spec(rng, out, out, 3, 1, 1, ta())]
+        else:  # bottleneck
+            mid = max(64, out // 4) if out >= 256 else 64
+            convs = [conv_spec(rng, c, mid, 1, 1, 0, ta()), conv_spec(rng, mid, mid, 3, stride, 1, ta()),
+                     conv_spec(rng, mid, out, 1, 1, 0, ta())]
+        blk = dict(convs=convs)
+        if stride != 1 or out != c:
+            blk["down"] = conv_spec(rng, c, out, 1, stride, 0, ta())
+        blocks.append(blk)
+        c, h = out, h // stride
+    n = int(rng.integers(1, 4))
+    h0 = h * 2 ** sum(1 for b in blocks if b.get("down") is not None and b["down"]["stride"] == 2)
+    x = np.abs(rng.standard_normal(n * 64 * h0 * h0)).astype(np.float32)
+    return blocks, (n, 64, h0, h0), x
+
+
+@pytest.mark.parametrize("seed", [101, 202, 303, 404])
+def test_fused_random_bodies(oracle, seed):
+    """Random block structures through the fused kernels (every tiling rule:
+    MT, column split, integer / DPX thresholds, resident vs streamed weights)
+    bit-exact against the oracle."""
+    blocks, (n, c, h, w), x = _random_body(seed)
+    _check(oracle, blocks, x, n, c, h, w, expect_fused=True)
+
+
 def test_fused_equals_generic(oracle):
     from paper_2008_05101_b200 import _lib as T
     blocks, (n, c, h, w), x = fused_small(seed=5, n=2, h=12, w=20)
