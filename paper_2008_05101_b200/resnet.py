@@ -297,7 +297,13 @@ class PipelinedResNet:
 
     def forward(self, images_host: torch.Tensor) -> torch.Tensor:
         cs = torch.cuda.current_stream()
-        self.copy_stream.wait_stream(cs)  # previous users of the outputs are ordered
+        # Slice i's upload waits only for the previous call's stem of slice i
+        # (ev_consumed), not for the previous call's bodies: back-to-back calls
+        # overlap the next batch's upload with this batch's last body and head
+        # (the copy engine would otherwise idle through them).  The first call
+        # orders its uploads after the caller's earlier work on this stream.
+        if self._first:
+            self.copy_stream.wait_stream(cs)
         with torch.cuda.stream(self.copy_stream):
             for i in range(self.chunks):
                 if not self._first:  # the previous step's stem has read this buffer

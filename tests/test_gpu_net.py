@@ -238,6 +238,16 @@ def test_pipelined_e2e_matches_serial_chunks(tk):
     got_g = pipe_g.forward(imgs).clone()
     torch.cuda.synchronize()
     assert torch.equal(pipe_g.pooled, pooled) and torch.equal(got_g, got)
+    # back-to-back calls without a host sync (the next upload overlaps this
+    # call's last body and head): each call's logits are its own
+    imgs2 = torch.rand(16, 3, 224, 224, generator=g).pin_memory()
+    want2 = pipe.forward(imgs2).clone()
+    torch.cuda.synchronize()
+    outs = []
+    for im in (imgs, imgs2, imgs, imgs2):
+        outs.append(pipe.forward(im).clone())
+    torch.cuda.synchronize()
+    assert all(torch.equal(o, w) for o, w in zip(outs, (got, want2, got, want2)))
     # uneven slices (4 + 8 + 4 images), bodies on 12 + 4 images: the same bits
     pipe_u = PipelinedResNet(net, 16, groups=[2, 1], slices=[4, 8, 4])
     got_u = pipe_u.forward(imgs).clone()
