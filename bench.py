@@ -628,16 +628,15 @@ class ResNetWorkload:
         self.pooled = torch.empty((batch, self.net.body.out_shape[0]), device="cuda")
         self.logits_host = torch.empty((global_batch if rank == 0 else 0, 1000)).pin_memory()
         # e2e: chunked so the image upload overlaps the compute of earlier chunks
-        # (tools/e2e_groups.py, tensor-core stem: R18 b256 -- upload-bound --
-        # 8 slices with the body on 2+2+2+2 slices 3.30 ms, 3+5 3.70, 1 x 8
-        # 4.13; R50 b1024 -- compute-bound, so start early and grow --
-        # 16 slices on 1+2+5+8 21.3 ms, 8 slices on 3+5 22.9, 2+2+2+2 23.6)
+        # and consecutive steps overlap (tools/e2e_groups.py: R18 b256 --
+        # upload-bound -- 8 slices with the body on 2+2+2+2 slices, 2.84 ms =
+        # the PCIe time of 154 MB; R50 b1024 -- compute-bound, the next upload
+        # hides under this body -- one body over 4 slices 19.4 ms, 8 slices on
+        # 3+5 19.6, 16 on 1+2+5+8 20.5)
         if batch % 8 == 0 and 128 <= batch <= 256:
             chunks, groups = 8, [2, 2, 2, 2]
-        elif batch % 16 == 0 and batch > 256:
-            chunks, groups = 16, [1, 2, 5, 8]
-        elif batch % 8 == 0 and batch > 256:
-            chunks, groups = 8, [3, 5]
+        elif batch % 4 == 0 and batch > 256:
+            chunks, groups = 4, [4]
         elif batch % 4 == 0 and batch >= 64:
             chunks, groups = 4, [2, 2]
         else:
